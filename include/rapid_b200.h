@@ -1,0 +1,103 @@
+/*
+ * rapid_b200.h — C ABI of the B200-native RAPID-Serve hot path
+ * (librapid_b200.so, built from paper_2601_11822_b200/csrc/).
+ *
+ * The reference (arxiv/paper_2601_11822, a pure-Python simulator) has no
+ * native code; its GPU work is a price returned by pure functions. Each entry
+ * point below is the physical realization of one of those prices and cites the
+ * reference interface it replaces (paths relative to /root/reference/).
+ *
+ * Conventions
+ *  - Plain pointers are device pointers unless stated; sizes are element counts.
+ *  - `stream` is a cudaStream_t (CUstream) — e.g. torch.cuda.current_stream()
+ *    .cuda_stream or a green-context stream from rb_green_split().
+ *  - Every call is asynchronous and stream-ordered; nothing synchronizes.
+ *  - Return value: 0 on success, non-zero on error; rb_last_error() returns a
+ *    thread-local message. Argument errors never launch anything.
+ *  - bf16 tensors are row-major; `ld*` are row strides in elements.
+ *  - Paged KV cache, one layer: [num_blocks][2 (K,V)][Hkv][16][head_dim] bf16.
+ *  - Block table: int32 [num_slots][bt_stride]; a request occupies one slot.
+ */
+#ifndef RAPID_B200_H
+#define RAPID_B200_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Library identity / diagnostics. */
+const char* rb_version(void);
+const char* rb_last_error(void);
+int rb_device_sm_count(int device, int* out);
+/* Debug: when buf != NULL, every GEMM CTA writes 8 globaltimer stamps to buf[8*cta..]. */
+int rb_debug_gemm_trace(unsigned long long* buf);
+
+/* K1/K4 — bf16 linear layer on tcgen05 tensor cores:
+ *   Y[t,o] = sum_k X[t,k] W[o,k] (+bias[o]) (+R[t,o])
+ * Replaces the compute term of prefill_time (pkg/src/pdsim/costmodel.py:104)
+ * and the weight-streaming term of decode_time (costmodel.py:130).
+ * mode: 0 auto, 1 token-major tiles (prefill), 2 swap-AB (decode, T<=256).
+ * num_sms: SMs of the partition the stream runs on (persistent grid size).
+ * workspace/counters: split-K scratch (fp32) and zeroed int32 tile counters;
+ * may be NULL (no split-K). R may alias Y (in-place residual add). */
+int rb_gemm_bf16(const void* X, const void* W, void* Y, const void* bias, const void* R, int T, int O, int K,
+                 long long ldx, long long ldw, long long ldy, int mode, int num_sms, void* workspace,
+                 size_t ws_bytes, int* counters, int counters_len, void* stream);
+
+/* K3 — decode paged attention, one query token per row:
+ *   out[b,h,:] = softmax(scale * q[b,h,:] . K[slot_b, :seq_lens[b]]) V
+ * Replaces the KV-read term kv_cache_bytes(model, total_kv_tokens) of
+ * decode_time (costmodel.py:131). row_slot[b] selects the block-table row;
+ * rows with seq_lens[b] <= 0 are skipped (graph padding). splits > 1 needs
+ * workspace of B*Hq*splits*(head_dim+2)*4 bytes. */
+int rb_decode_attention(const void* q, long long q_tok_stride, const void* cache_layer, const int* block_table,
+                        int bt_stride, const int* row_slot, const int* seq_lens, void* out,
+                        long long out_tok_stride, void* workspace, size_t ws_bytes, int B, int Hq, int Hkv,
+                        int head_dim, int splits, float scale, void* stream);
+
+/* K2 — causal prefill attention of one chunk (positions start..start+T-1)
+ * against the paged cache [0, start+T). Replaces the attention share of
+ * prefill_time's compute term (costmodel.py:104) for the chunk priced at
+ * pkg/src/pdsim/engines/rapid.py:313. */
+int rb_prefill_attention(const void* q, long long q_tok_stride, const void* cache_layer, const int* block_table_row,
+                         int T, int start, int Hq, int Hkv, int head_dim, void* out, long long out_tok_stride,
+                         float scale, void* stream);
+
+/* K5 — RoPE on q,k + paged KV write of k,v for T rows (pos[t] < 0 skips).
+ * Replaces the KV-write term kv_cache_bytes(model, tokens) of prefill_time
+ * (costmodel.py:105) and kv_cache_bytes(model, batch) of decode_time (:132).
+ * cos_sin: fp32 [max_pos][head_dim] = [cos | sin]. */
+int rb_rope_cache_write(const void* qkv, long long ld_qkv, const int* pos, const int* tok_slot,
+                        const int* block_table, int bt_stride, const float* cos_sin, void* q_out, long long ld_q,
+                        void* cache_layer, int T, int Hq, int Hkv, int head_dim, void* stream);
+
+/* K5 — small fused ops (part of fixed_iteration_overhead_us, costmodel.py:53). */
+int rb_rmsnorm(const void* x, long long ldx, const void* w, void* y, long long ldy, int T, int H, float eps,
+               void* stream);
+int rb_silu_mul(const void* gate_up, long long ld_gu, void* y, long long ldy, int T, int I, void* stream);
+int rb_embed(const int* ids, const int* slot_of_row, const int* last_tok, const void* table, void* y, int T, int H,
+             int* ids_out, void* stream);
+int rb_argmax(const void* logits, long long ld, int T, int V, int* out, const int* slot_of_row, int* last_tok,
+              const int* row_valid, void* stream);
+
+/* Device-side block-table maintenance (BlockPool physical IDs,
+ * pkg/src/pdsim/kvcache.py:85-127): upd = [count, (slot, idx, block)*count]. */
+int rb_block_table_update(const int* upd, int* block_table, int bt_stride, int max_updates, void* stream);
+int rb_set_last_token(int* last_tok, int slot, const int* value_ptr, int value, void* stream);
+
+/* K7 — SM partitioning with CUDA green contexts (replaces the CU-fraction
+ * scalars of AllocationDecision, pkg/src/pdsim/core.py:215-245, and the
+ * cu_fraction argument of effective_bandwidth/_roofline_us,
+ * costmodel.py:62-86). Splits the device into a group of >= first_sms SMs and
+ * the remainder; returns one non-blocking stream bound to each partition and
+ * the actual SM counts. handle is released by rb_green_destroy. */
+int rb_green_split(int device, int first_sms, void** handle, void** stream_first, void** stream_second,
+                   int* sms_first, int* sms_second);
+int rb_green_destroy(void* handle);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RAPID_B200_H */

@@ -1,0 +1,354 @@
+// K1 / K4: bf16 "linear" GEMM on 5th-gen tensor cores (tcgen05 + TMEM + TMA).
+//
+//   Y[t, o] = sum_k X[t, k] * W[o, k]  (+ bias[o]) (+ R[t, o])
+//
+// Realizes the compute term of prefill_time / the weight term of decode_time
+// (reference pkg/src/pdsim/costmodel.py:104 and :130).
+//
+// Two operand mappings onto the UMMA M=128 x N=BN tile:
+//   normal  (prefill, many tokens): MMA-M = tokens t, MMA-N = features o.
+//   swap-AB (decode, M=B <= 256):   MMA-M = features o, MMA-N = tokens t,
+//            so the tiny batch becomes the UMMA N dimension and the weight
+//            matrix streams through the 128-row A operand (HBM-bound path).
+// Both operands are K-major; TMA loads 64-element (128 B) K slabs with the
+// 128B swizzle straight into the UMMA smem layout.
+//
+// Warp roles (192 threads): w0 = TMA producer, w1 = TMEM owner + MMA issuer,
+// w2..w5 = epilogue. Persistent grid, static stride tile schedule, 2 TMEM
+// accumulator buffers so the epilogue of tile i overlaps the MMAs of tile i+1.
+// Epilogue: TMEM -> registers -> per-warp smem tile in OUTPUT orientation ->
+// 16-byte coalesced global stores (8 rows x 64 B per warp instruction), with
+// bias / residual fused in the write-out pass; the same code serves both
+// mappings (swap-AB transposes while staging).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include "ptx.cuh"
+#include "rb_common.h"
+
+namespace rb {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;                 // bf16 elements per 128-byte swizzle row
+constexpr int kABytes = kBM * kBK * 2;  // 16 KB
+constexpr int kThreads = 192;
+constexpr int kStgStride = 40;          // bf16 per staging row (32 + 8 pad, 80 B)
+constexpr int kStgBytes = 32 * kStgStride * 2;  // per epilogue warp
+
+struct GemmArgs {
+  int m_tiles, n_tiles, num_kb, total_tiles;
+  int BN, stages;
+  int M_valid, N_valid;  // extents in MMA space
+  int swap;              // 1: MMA-M = features (output columns), MMA-N = tokens (output rows)
+  long long ldy;
+  __nv_bfloat16* out;
+  const __nv_bfloat16* residual;
+  const __nv_bfloat16* bias;
+  uint64_t hint_a, hint_b;
+};
+
+// Optional timeline trace (debug): per CTA 8 globaltimer stamps.
+__device__ unsigned long long* g_gemm_trace = nullptr;
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(slot)                                                     \
+  do {                                                                  \
+    if (g_gemm_trace) g_gemm_trace[blockIdx.x * 8 + (slot)] = gtime(); \
+  } while (0)
+
+// One warp's 32 (MMA rows) x 32 (MMA cols) accumulator block -> Y.
+__device__ __forceinline__ void epi_block(const GemmArgs& g, __nv_bfloat16* stg, int lane, int m0, int n0,
+                                          const uint32_t (&v)[32]) {
+  if (!g.swap) {
+    uint4* dst = reinterpret_cast<uint4*>(stg + lane * kStgStride);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      dst[k] = make_uint4(pack_bf16x2(__uint_as_float(v[8 * k + 0]), __uint_as_float(v[8 * k + 1])),
+                          pack_bf16x2(__uint_as_float(v[8 * k + 2]), __uint_as_float(v[8 * k + 3])),
+                          pack_bf16x2(__uint_as_float(v[8 * k + 4]), __uint_as_float(v[8 * k + 5])),
+                          pack_bf16x2(__uint_as_float(v[8 * k + 6]), __uint_as_float(v[8 * k + 7])));
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) stg[j * kStgStride + lane] = __float2bfloat16_rn(__uint_as_float(v[j]));
+  }
+  __syncwarp();
+  const int row0 = g.swap ? n0 : m0;  // output row (token) base
+  const int col0 = g.swap ? m0 : n0;  // output col (feature) base
+  const int rows_valid = g.swap ? g.N_valid : g.M_valid;
+  const int cols_valid = g.swap ? g.M_valid : g.N_valid;
+  const int cs = (lane & 3) * 8;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = i * 8 + (lane >> 2);
+    const int row = row0 + r;
+    const int col = col0 + cs;
+    if (row >= rows_valid || col >= cols_valid) continue;
+    const uint4 sv = *reinterpret_cast<const uint4*>(stg + r * kStgStride + cs);
+    float x[8];
+    {
+      const uint32_t w[4] = {sv.x, sv.y, sv.z, sv.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float2 f = unpack_bf16x2(w[j]);
+        x[2 * j] = f.x;
+        x[2 * j + 1] = f.y;
+      }
+    }
+    __nv_bfloat16* dst = g.out + (long long)row * g.ldy + col;
+    if (col + 8 <= cols_valid) {
+      if (g.bias) {
+        const uint4 b = *reinterpret_cast<const uint4*>(g.bias + col);
+        const uint32_t w[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float2 f = unpack_bf16x2(w[j]);
+          x[2 * j] += f.x;
+          x[2 * j + 1] += f.y;
+        }
+      }
+      if (g.residual) {
+        const uint4 rr = *reinterpret_cast<const uint4*>(g.residual + (long long)row * g.ldy + col);
+        const uint32_t w[4] = {rr.x, rr.y, rr.z, rr.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float2 f = unpack_bf16x2(w[j]);
+          x[2 * j] += f.x;
+          x[2 * j + 1] += f.y;
+        }
+      }
+      *reinterpret_cast<uint4*>(dst) = make_uint4(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3]),
+                                                  pack_bf16x2(x[4], x[5]), pack_bf16x2(x[6], x[7]));
+    } else {
+      for (int j = 0; j < 8 && col + j < cols_valid; ++j) {
+        float y = x[j];
+        if (g.bias) y += __bfloat162float(g.bias[col + j]);
+        if (g.residual) y += __bfloat162float(g.residual[(long long)row * g.ldy + col + j]);
+        dst[j] = __float2bfloat16_rn(y);
+      }
+    }
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                             const __grid_constant__ CUtensorMap tmap_b, const GemmArgs g) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int BN = g.BN;
+  const int stages = g.stages;
+  const uint32_t b_bytes = (uint32_t)BN * kBK * 2;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + (size_t)stages * kABytes;
+  __nv_bfloat16* stg_all = reinterpret_cast<__nv_bfloat16*>(sB + (size_t)stages * b_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stg_all) + 4 * kStgBytes);
+  uint64_t* empty = full + stages;
+  uint64_t* tfull = empty + stages;  // 2
+  uint64_t* tempty = tfull + 2;      // 2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t acc_stride = (uint32_t)BN;
+  uint32_t tmem_cols = 32;
+  while (tmem_cols < 2 * acc_stride) tmem_cols <<= 1;
+
+  if (threadIdx.x == 0) TRACE(0);
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b);
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) TRACE(1);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ================= TMA producer =================
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
+        const int mt = t % g.m_tiles;
+        const int nt = t / g.m_tiles;
+        for (int kb = 0; kb < g.num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], kABytes + b_bytes);
+          tma_load_2d(sA + (size_t)stage * kABytes, &tmap_a, &full[stage], kb * kBK, mt * kBM, g.hint_a);
+          tma_load_2d(sB + (size_t)stage * b_bytes, &tmap_b, &full[stage], kb * kBK, nt * BN, g.hint_b);
+          if (++stage == stages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ================= MMA issuer (single thread) =================
+      const uint32_t idesc = make_idesc_bf16(kBM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)acc * acc_stride;
+        for (int kb = 0; kb < g.num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          if (t == (int)blockIdx.x && kb == 0) TRACE(2);
+          if (t == (int)blockIdx.x && kb == g.num_kb - 1) TRACE(3);
+          tc_fence_after();
+          const uint64_t adesc = make_sdesc_sw128(sA + (size_t)stage * kABytes);
+          const uint64_t bdesc = make_sdesc_sw128(sB + (size_t)stage * b_bytes);
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            // advance 16 elements (32 bytes) inside the swizzle atom: +2 in 16-byte units
+            umma_bf16(d_tmem, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2), idesc,
+                      (kb > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == stages) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // ================= epilogue warps 2..5 =================
+    const int q = warp & 3;  // TMEM lane quadrant accessible by this warp
+    __nv_bfloat16* stg = stg_all + (size_t)q * (kStgBytes / 2);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
+      const int mt = t % g.m_tiles;
+      const int nt = t / g.m_tiles;
+      const int m0 = mt * kBM + q * 32;
+      mbar_wait(&tfull[acc], acc_phase);
+      if (lane == 0 && q == 0 && t == (int)blockIdx.x) TRACE(4);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)acc * acc_stride;
+      if (m0 < g.M_valid) {
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(tbase + c, v);
+          tmem_ld_wait();
+          if (nt * BN + c < g.N_valid) epi_block(g, stg, lane, m0, nt * BN + c, v);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0 && q == 0 && t == (int)blockIdx.x) TRACE(5);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) TRACE(6);
+  if (warp == 1) {
+    __syncwarp();
+    tmem_dealloc(tmem_base, tmem_cols);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+
+int gemm_set_trace(unsigned long long* buf) {
+  cudaError_t e = cudaMemcpyToSymbol(g_gemm_trace, &buf, sizeof(buf));
+  return e == cudaSuccess ? 0 : set_cuda_error("gemm trace", e);
+}
+
+static int gemm_smem_bytes(int bn, int stages) {
+  return stages * (kABytes + bn * kBK * 2) + 4 * kStgBytes + 1024 /*align*/ + (2 * stages + 4) * 8 + 16;
+}
+
+int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, const void* residual, int T,
+                     int O, int K, long long ldx, long long ldw, long long ldy, int mode, int num_sms,
+                     void* workspace, size_t ws_bytes, int* counters, int counters_len, cudaStream_t stream) {
+  (void)workspace; (void)ws_bytes; (void)counters; (void)counters_len;  // split-K scratch: reserved
+  if (T <= 0 || O <= 0) return 0;
+  if (K % kBK != 0) return set_error("gemm: K must be a multiple of 64");
+  if ((ldx * 2) % 16 || (ldw * 2) % 16) return set_error("gemm: row strides must be 16-byte multiples");
+  if (reinterpret_cast<uintptr_t>(X) % 16 || reinterpret_cast<uintptr_t>(W) % 16)
+    return set_error("gemm: operands must be 16-byte aligned");
+  if (ldy % 8 || reinterpret_cast<uintptr_t>(Y) % 16 || (residual && reinterpret_cast<uintptr_t>(residual) % 16) ||
+      (bias && reinterpret_cast<uintptr_t>(bias) % 16))
+    return set_error("gemm: Y/residual/bias must be 16-byte aligned with ldy % 8 == 0");
+  if (mode == 0) mode = (T <= 256) ? 2 : 1;
+  const bool swap = (mode == 2);
+  GemmArgs g{};
+  const int M = swap ? O : T;  // MMA-space rows
+  const int N = swap ? T : O;  // MMA-space cols
+  int BN;
+  if (swap) {
+    BN = ((N + 31) / 32) * 32;
+    if (BN > 256) BN = 256;
+  } else {
+    BN = 256;
+  }
+  const int stage_bytes = kABytes + BN * kBK * 2;
+  int stages = (200 * 1024 - 4 * kStgBytes) / stage_bytes;
+  if (stages > 8) stages = 8;
+  if (stages < 2) stages = 2;
+  g.BN = BN;
+  g.stages = stages;
+  g.m_tiles = (M + kBM - 1) / kBM;
+  g.n_tiles = (N + BN - 1) / BN;
+  g.num_kb = K / kBK;
+  g.total_tiles = g.m_tiles * g.n_tiles;
+  g.M_valid = M;
+  g.N_valid = N;
+  g.swap = swap ? 1 : 0;
+  g.ldy = ldy;
+  g.out = reinterpret_cast<__nv_bfloat16*>(Y);
+  g.residual = reinterpret_cast<const __nv_bfloat16*>(residual);
+  g.bias = reinterpret_cast<const __nv_bfloat16*>(bias);
+  if (swap) {
+    g.hint_a = kEvictFirst;  // weights stream once
+    g.hint_b = kEvictLast;   // activations reused by every weight tile
+  } else {
+    g.hint_a = kEvictLast;
+    g.hint_b = kEvictNormal;
+  }
+  if (num_sms <= 0) num_sms = 148;
+
+  CUtensorMap ta, tb;
+  const void* a_ptr = swap ? W : X;
+  const void* b_ptr = swap ? X : W;
+  const long long lda = swap ? ldw : ldx;
+  const long long ldb = swap ? ldx : ldw;
+  int rc = make_tmap_2d_bf16(&ta, a_ptr, (uint64_t)K, (uint64_t)M, (uint64_t)lda, kBK, kBM);
+  if (rc) return rc;
+  rc = make_tmap_2d_bf16(&tb, b_ptr, (uint64_t)K, (uint64_t)N, (uint64_t)ldb, kBK, BN);
+  if (rc) return rc;
+
+  const int smem = gemm_smem_bytes(BN, stages);
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tcgen05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024);
+    if (e != cudaSuccess) return set_cuda_error("gemm: set smem attr", e);
+    attr_done = true;
+  }
+  int grid = g.total_tiles < num_sms ? g.total_tiles : num_sms;
+  gemm_bf16_tcgen05_kernel<<<grid, kThreads, smem, stream>>>(ta, tb, g);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error("gemm launch", e);
+  return 0;
+}
+
+}  // namespace rb

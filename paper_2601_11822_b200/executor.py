@@ -1,0 +1,104 @@
+"""The Executor boundary: who performs the GPU work an engine launches.
+
+The reference prices every iteration at its two launch sites
+(pkg/src/pdsim/engines/rapid.py:173-189 prefill, :267-293 decode;
+hybrid.py:127 fused). Here those sites call an Executor instead:
+
+  launch_prefill(req, written, chunk, target, decision, co_decode) -> handle
+  launch_decode(members, decision, co_prefill_chunk)               -> handle
+  launch_hybrid(members, head, written, chunk, target)             -> handle
+  finish_decode(handle) / finish_prefill(handle) / finish_hybrid(handle)
+  on_preempt(req) / on_finish(req) / bind(engine)
+
+A handle carries `gpu_us` (known at launch for the cost model, filled at
+completion on the GPU) and `done()`.
+
+`CostModelExecutor` re-creates the reference's pricing decisions exactly, so
+`RapidEngine` + `CostModelExecutor` under `Simulation` reproduces the
+reference schedules bit for bit. `B200Executor` (executor_b200.py) launches
+real kernels on green-context streams.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from paper_2601_11822_b200.arm import decode_time, hybrid_time, overlapped_times, prefill_time
+from paper_2601_11822_b200.specs import OVERALLOCATE, AllocationDecision, AllocationMode
+
+
+@dataclass
+class PricedHandle:
+    gpu_us: int
+    cu_fraction: float
+    kind: str
+    members: tuple = ()
+
+    def done(self) -> bool:
+        return True
+
+
+class CostModelExecutor:
+    """Device = the reference's two-term roofline (costmodel.py:89-250)."""
+
+    realtime = False
+
+    def bind(self, engine) -> None:
+        self.engine = engine
+        self.model = engine.model
+        self.gpu = engine.gpu
+        self.params = engine.params
+
+    # RAPID prefill site (rapid.py:171-189)
+    def launch_prefill(self, req, written: int, chunk: int, target: int, decision: AllocationDecision,
+                       co_decode: tuple[int, int] | None) -> PricedHandle:
+        m, g, p = self.model, self.gpu, self.params
+        if decision.mode is AllocationMode.PARTITION:
+            cu = decision.cu_fraction_prefill
+            us = prefill_time(chunk, cu, m, g, p, concurrent=co_decode is not None)
+        else:
+            cu = 1.0
+            if co_decode is not None:
+                us = overlapped_times(chunk, co_decode[0], co_decode[1], OVERALLOCATE, m, g, p)[0]
+            else:
+                us = prefill_time(chunk, 1.0, m, g, p)
+        return PricedHandle(us, cu, "prefill")
+
+    # RAPID decode site (rapid.py:266-293)
+    def launch_decode(self, members, decision: AllocationDecision, co_prefill_chunk: int | None) -> PricedHandle:
+        m, g, p = self.model, self.gpu, self.params
+        batch = len(members)
+        total_kv = sum(r.context_tokens for r in members)
+        if decision.mode is AllocationMode.PARTITION:
+            cu = decision.cu_fraction_decode
+            us = decode_time(batch, total_kv, cu, m, g, p, concurrent=co_prefill_chunk is not None)
+        else:
+            cu = 1.0
+            if co_prefill_chunk is not None:
+                us = overlapped_times(co_prefill_chunk, batch, total_kv, OVERALLOCATE, m, g, p)[1]
+            else:
+                us = decode_time(batch, total_kv, 1.0, m, g, p)
+        h = PricedHandle(us, cu, "decode", tuple(members))
+        h.total_kv = total_kv
+        return h
+
+    # hybrid fused site (hybrid.py:126-127)
+    def launch_hybrid(self, members, head, written: int, chunk: int, target: int) -> PricedHandle:
+        total_kv = sum(r.context_tokens for r in members) + written
+        return PricedHandle(hybrid_time(chunk, len(members), total_kv, self.model, self.gpu, self.params), 1.0,
+                            "hybrid", tuple(members))
+
+    def finish_prefill(self, handle) -> None:
+        pass
+
+    def finish_decode(self, handle) -> None:
+        pass
+
+    def finish_hybrid(self, handle) -> None:
+        pass
+
+    def on_preempt(self, req) -> None:
+        pass
+
+    def on_finish(self, req) -> None:
+        pass
