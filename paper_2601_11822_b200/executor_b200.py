@@ -1,0 +1,378 @@
+"""B200Executor: the engines' launch sites realized as sm_100a kernels.
+
+RAPID (engines/rapid.py) calls launch_prefill / launch_decode exactly where the
+reference prices an iteration (pkg/src/pdsim/engines/rapid.py:171-189,
+:266-293); completions come back through CUDA events polled by RealTimeLoop.
+
+Phases and SM partitions (K7): the ARM decision selects the streams —
+  * OVERALLOCATE: both phases on full-device streams (148 SMs, contending);
+  * PARTITION:    decode on a green context of cu_fraction_decode*148 SMs
+                  rounded up to 8, prefill on the complementary green context.
+A static split (cfg 2) fixes one partition for the whole run.
+
+Token-position contract: a prefill of `target`
+context tokens computes KV for positions 0..target-2 only; decode
+participation k consumes the token at position target-2+k (its input id
+lives in last_tok[slot] on the device) and writes its KV there.
+
+Block-table mirroring: the BlockPool reports every new page; admission pages
+are applied on the prefill stream before that request's first chunk, decode
+extensions on the decode stream before the step that needs them.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+
+import torch
+
+from paper_2601_11822_b200 import ops
+from paper_2601_11822_b200.arm import DEFAULT_BATCH_GRID
+from paper_2601_11822_b200.blockpool import BlockPool
+from paper_2601_11822_b200.model import PAGE, DecoderWeights, Runner
+from paper_2601_11822_b200.specs import AllocationDecision, AllocationMode, ArchConfig, decode_sms_for
+from paper_2601_11822_b200.traffic import prompt_token_ids
+
+MAX_UPDATES = 1 << 16
+
+
+class GpuHandle:
+    __slots__ = ("kind", "ev0", "ev1", "gpu_us", "cu_fraction", "members", "start_us", "lame", "rows", "launch_ns",
+                 "req", "last_chunk")
+
+    def __init__(self, kind, stream, cu_fraction):
+        self.kind = kind
+        self.ev0 = torch.cuda.Event(enable_timing=True)
+        self.ev1 = torch.cuda.Event(enable_timing=True)
+        self.ev0.record(stream)
+        self.gpu_us = 0
+        self.cu_fraction = cu_fraction
+        self.members = ()
+        self.start_us = 0
+        self.launch_ns = time.perf_counter_ns()
+
+    def finish_record(self, stream):
+        self.ev1.record(stream)
+
+    def done(self) -> bool:
+        if self.ev1.query():
+            self.gpu_us = max(1, int(round(self.ev0.elapsed_time(self.ev1) * 1000.0)))
+            return True
+        return False
+
+
+class _Partition:
+    """A pair of streams (decode, prefill) with their SM counts."""
+
+    def __init__(self, decode_stream, prefill_stream, decode_sms, prefill_sms, green=None):
+        self.ds = decode_stream
+        self.ps = prefill_stream
+        self.d_sms = decode_sms
+        self.p_sms = prefill_sms
+        self.green = green
+        self.graphs: dict[int, torch.cuda.CUDAGraph] = {}
+
+
+class B200Executor:
+    realtime = True
+
+    def __init__(self, arch: ArchConfig, weights: DecoderWeights | None = None, *, seed: int = 0,
+                 static_decode_sms: int | None = None, max_batch: int = 256, chunk_tokens: int = 2048,
+                 num_blocks: int | None = None, kv_memory_fraction: float = 0.90, max_context: int | None = None,
+                 num_slots: int = 1024, device: str = "cuda", token_source=None, use_graphs: bool = True,
+                 batch_grid: tuple[int, ...] = DEFAULT_BATCH_GRID, serialize_phases: bool = False):
+        self.arch = arch
+        dev = torch.device(device)
+        self.device = dev if dev.index is not None else torch.device("cuda", torch.cuda.current_device())
+        torch.cuda.set_device(self.device)
+        ops.load()
+        self.weights = weights if weights is not None else DecoderWeights.random(arch, device=self.device, seed=seed)
+        self.max_batch = max_batch
+        self.chunk_tokens = chunk_tokens
+        self.num_slots = num_slots
+        self.use_graphs = use_graphs
+        self.grid = tuple(b for b in batch_grid if b <= max_batch) or (max_batch,)
+        if self.grid[-1] < max_batch:
+            self.grid = self.grid + (max_batch,)
+        self.total_sms = ops.device_sm_count(self.device.index or 0)
+        self.token_source = token_source or (lambda req: prompt_token_ids(req.id, req.prompt_tokens, arch.vocab))
+        max_ctx = max_context or 16384
+        self.max_blocks_per_seq = (max_ctx + PAGE) // PAGE + 1
+        bpb = Runner.kv_bytes_per_block(arch)
+        if num_blocks is None:
+            torch.cuda.synchronize()
+            free, _ = torch.cuda.mem_get_info(self.device)
+            # activations / graphs / workspaces: reserve generously, then the reference's 10% rule
+            act = self._activation_bytes(max(chunk_tokens, 1), max_batch) + (2 << 30)
+            num_blocks = int(max(0, free - act) * kv_memory_fraction // bpb)
+        if num_blocks < 1:
+            raise RuntimeError("no HBM left for the KV cache")
+        self.num_blocks = num_blocks
+        self.runner = Runner(self.weights, num_blocks, num_slots, self.max_blocks_per_seq,
+                             max_prefill_tokens=max(chunk_tokens, 16), max_decode_batch=max_batch, device=self.device)
+        # host mirrors / staging (pinned)
+        self._slot_of: dict[int, int] = {}
+        self._free_slots = list(range(num_slots - 1, -1, -1))
+        self._upd = {"prefill": [], "decode": []}
+        self._upd_host = {k: torch.zeros(1 + 3 * MAX_UPDATES, dtype=torch.int32, pin_memory=True)
+                          for k in self._upd}
+        self._upd_dev = {k: torch.zeros(1 + 3 * MAX_UPDATES, dtype=torch.int32, device=self.device)
+                         for k in self._upd}
+        self._dec_in_host = torch.zeros(3, max_batch, dtype=torch.int32, pin_memory=True)
+        self._dec_in_dev = torch.zeros(3, max_batch, dtype=torch.int32, device=self.device)
+        d = self.runner.dec
+        d.slot = self._dec_in_dev[0]
+        d.pos = self._dec_in_dev[1]
+        d.seq = self._dec_in_dev[2]
+        self._dec_out_host = torch.zeros(max_batch, dtype=torch.int32, pin_memory=True)
+        self._pre_ids_host = torch.zeros(max(chunk_tokens, 16), dtype=torch.int32, pin_memory=True)
+        self._pre_ids_dev = torch.zeros(max(chunk_tokens, 16), dtype=torch.int32, device=self.device)
+        self.generated: dict[int, list[int]] = {}
+        self._tokens_cache: dict[int, torch.Tensor] = {}
+        # partitions
+        self._partitions: dict[int | None, _Partition] = {}
+        full_d = torch.cuda.Stream(device=self.device)
+        full_p = full_d if serialize_phases else torch.cuda.Stream(device=self.device)
+        self._partitions[None] = _Partition(full_d, full_p, self.total_sms, self.total_sms)
+        self.static_decode_sms = static_decode_sms
+        if static_decode_sms is not None:
+            self._partition(static_decode_sms)
+        # stats
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+        self.decode_steps = 0
+        self.prefill_chunks = 0
+        self.gpu_launches = 0
+        self.step_log: list[tuple[int, int, int]] = []  # (B, gpu_us, host launch ns)
+
+    # ------------------------------------------------------------------ sizing
+    def _activation_bytes(self, T: int, B: int) -> int:
+        a = self.arch
+        nq = (a.q_heads + 2 * a.kv_heads) * a.head_dim
+        per_row = 2 * (2 * a.hidden + nq + 2 * a.q_heads * a.head_dim + 3 * a.intermediate)
+        return per_row * (T + B) + B * a.vocab * 2 + B * a.q_heads * 16 * (a.head_dim + 2) * 4
+
+    def make_pool(self, model, gpu) -> BlockPool:
+        pool = BlockPool(self.num_blocks, PAGE, name="gpu0")
+        pool.listener = self
+        return pool
+
+    def bind(self, engine) -> None:
+        self.engine = engine
+        if getattr(engine, "max_batch", self.max_batch) > self.max_batch:
+            raise ValueError("engine max_batch exceeds the executor's decode workspace")
+
+    # ------------------------------------------------------------------ partitions
+    def _partition(self, decode_sms: int | None) -> _Partition:
+        if decode_sms not in self._partitions:
+            gs = ops.GreenSplit(decode_sms, device=self.device.index or 0)
+            self._partitions[decode_sms] = _Partition(gs.streams[0], gs.streams[1], gs.sms[0], gs.sms[1], gs)
+        return self._partitions[decode_sms]
+
+    def _pick(self, decision: AllocationDecision) -> _Partition:
+        if self.static_decode_sms is not None:
+            return self._partitions[self.static_decode_sms]
+        return self._partition(decode_sms_for(decision, self.total_sms))
+
+    # ------------------------------------------------------------------ pool listener
+    def _slot(self, req_id: int) -> int:
+        s = self._slot_of.get(req_id)
+        if s is None:
+            if not self._free_slots:
+                raise RuntimeError("out of request slots")
+            s = self._free_slots.pop()
+            self._slot_of[req_id] = s
+        return s
+
+    def on_pages(self, req_id: int, first_index: int, ids: list[int]) -> None:
+        s = self._slot(req_id)
+        if first_index + len(ids) > self.max_blocks_per_seq:
+            raise RuntimeError("request context exceeds max_blocks_per_seq")
+        q = self._upd["prefill" if first_index == 0 else "decode"]
+        for j, b in enumerate(ids):
+            q.append((s, first_index + j, b))
+
+    def on_release(self, req_id: int) -> None:
+        s = self._slot_of.pop(req_id, None)
+        if s is not None:
+            self._free_slots.append(s)
+
+    def _flush_updates(self, phase: str, stream) -> None:
+        q = self._upd[phase]
+        if not q:
+            return
+        n = len(q)
+        if n > MAX_UPDATES:
+            raise RuntimeError("too many pending block-table updates")
+        h = self._upd_host[phase]
+        h[0] = n
+        flat = torch.tensor(q, dtype=torch.int32).view(-1)
+        h[1 : 1 + 3 * n].copy_(flat)
+        d = self._upd_dev[phase]
+        with torch.cuda.stream(stream):
+            d[: 1 + 3 * n].copy_(h[: 1 + 3 * n], non_blocking=True)
+        ops.block_table_update(d, self.runner.block_table, n, stream=stream)
+        self.h2d_bytes += 4 * (1 + 3 * n)
+        self.gpu_launches += 1
+        q.clear()  # one launch per phase is in flight, so the pinned buffer is free again at the next flush
+
+    # ------------------------------------------------------------------ tokens
+    def _token_seq(self, req) -> torch.Tensor:
+        t = self._tokens_cache.get(req.id)
+        if t is None:
+            t = self.token_source(req)
+            self._tokens_cache[req.id] = t
+        return t
+
+    def _context_ids(self, req, lo: int, hi: int) -> torch.Tensor:
+        """Token ids at context positions [lo, hi): prompt then generated tokens."""
+        prompt = self._token_seq(req)
+        P = prompt.shape[0]
+        if hi <= P:
+            return prompt[lo:hi]
+        gen = self.generated.get(req.id, [])
+        tail = torch.tensor(gen[max(0, lo - P) : hi - P], dtype=torch.int32)
+        if lo >= P:
+            return tail
+        return torch.cat([prompt[lo:P], tail])
+
+    # ------------------------------------------------------------------ prefill
+    def launch_prefill(self, req, written: int, chunk: int, target: int, decision, co_decode) -> GpuHandle:
+        part = self._pick(decision)
+        st = part.ps
+        sh = st.cuda_stream
+        h = GpuHandle("prefill", st, part.p_sms / self.total_sms)
+        self._flush_updates("prefill", st)
+        slot = self._slot_of[req.id]
+        lo, hi = written, min(written + chunk, target - 1)
+        if hi > lo:
+            ids = self._context_ids(req, lo, hi)
+            n = hi - lo
+            self._pre_ids_host[:n].copy_(ids)
+            with torch.cuda.stream(st):
+                self._pre_ids_dev[:n].copy_(self._pre_ids_host[:n], non_blocking=True)
+                self.runner.prefill(slot, self._pre_ids_dev[:n], lo, num_sms=part.p_sms, stream=sh)
+            self.h2d_bytes += 4 * n
+            self.gpu_launches += 2 + 9 * self.arch.layers
+        if written + chunk == target:
+            nxt = int(self._context_ids(req, target - 1, target)[0])
+            ops.set_last_token(self.runner.last_tok, slot, value=nxt, stream=sh)
+            self.gpu_launches += 1
+        h.finish_record(st)
+        h.req = req
+        self.prefill_chunks += 1
+        return h
+
+    def finish_prefill(self, handle) -> None:
+        pass
+
+    # ------------------------------------------------------------------ decode
+    def _bucket(self, B: int) -> int:
+        for g in self.grid:
+            if g >= B:
+                return g
+        return self.grid[-1]
+
+    def _capture(self, part: _Partition, bucket: int) -> torch.cuda.CUDAGraph:
+        g = part.graphs.get(bucket)
+        if g is not None:
+            return g
+        r = self.runner
+        splits = r.decode_splits(bucket, PAGE * self.max_blocks_per_seq, part.d_sms)
+        st = part.ds
+        # warm up outside capture (tensor-map cache, function attributes)
+        r.decode_body(bucket, num_sms=part.d_sms, splits=splits, stream=st.cuda_stream)
+        st.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            r.decode_body(bucket, num_sms=part.d_sms, splits=splits, stream=st.cuda_stream)
+        st.synchronize()
+        part.graphs[bucket] = g
+        return g
+
+    def warmup(self, decode_sms_list=None) -> None:
+        """Pre-capture decode graphs for every bucket on the partitions in use."""
+        if not self.use_graphs:
+            return
+        keys = decode_sms_list if decode_sms_list is not None else (
+            [self.static_decode_sms] if self.static_decode_sms is not None else [None])
+        # padding rows only: make the workspace inputs inert for the warm-up replays
+        self._dec_in_dev[0].fill_(self.runner.dummy_slot)
+        self._dec_in_dev[1].fill_(-1)
+        self._dec_in_dev[2].fill_(0)
+        for k in keys:
+            part = self._partition(k) if k is not None else self._partitions[None]
+            for b in self.grid:
+                self._capture(part, b)
+        torch.cuda.synchronize()
+
+    def launch_decode(self, members, decision, co_prefill_chunk) -> GpuHandle:
+        part = self._pick(decision)
+        st = part.ds
+        B = len(members)
+        bucket = self._bucket(B)
+        h = GpuHandle("decode", st, part.d_sms / self.total_sms)
+        self._flush_updates("decode", st)
+        hin = self._dec_in_host
+        slots, pos, seq = [], [], []
+        lame = []
+        for r in members:
+            ctx = r.context_tokens
+            slots.append(self._slot_of[r.id])
+            pos.append(ctx - 1)
+            seq.append(ctx)
+            lame.append(r.delivered_tokens >= r.output_tokens)
+        pad = bucket - B
+        if pad:
+            slots += [self.runner.dummy_slot] * pad
+            pos += [-1] * pad
+            seq += [0] * pad
+        hin[:, :bucket].copy_(torch.tensor([slots, pos, seq], dtype=torch.int32))
+        with torch.cuda.stream(st):
+            self._dec_in_dev[:, :bucket].copy_(hin[:, :bucket], non_blocking=True)
+            if self.use_graphs:
+                self._capture(part, bucket).replay()
+            else:
+                self.runner.decode_body(bucket, num_sms=part.d_sms,
+                                        splits=self.runner.decode_splits(bucket, max(seq), part.d_sms),
+                                        stream=st.cuda_stream)
+            self._dec_out_host[:B].copy_(self.runner.dec.out_ids[:B], non_blocking=True)
+        h.finish_record(st)
+        h.members = tuple(members)
+        h.lame = lame
+        self.h2d_bytes += 12 * bucket
+        self.d2h_bytes += 4 * B
+        self.decode_steps += 1
+        self.gpu_launches += 4 + 9 * self.arch.layers + 3
+        return h
+
+    def finish_decode(self, handle) -> None:
+        if handle is None:
+            return
+        out = self._dec_out_host[: len(handle.members)].tolist()
+        for r, is_lame, tok in zip(handle.members, handle.lame, out):
+            if not is_lame:
+                self.generated.setdefault(r.id, []).append(tok)
+        self.step_log.append((len(handle.members), handle.gpu_us, handle.launch_ns))
+
+    # ------------------------------------------------------------------ hybrid (K9 fused iteration)
+    def launch_hybrid(self, members, head, written, chunk, target):
+        raise NotImplementedError("hybrid GPU iteration: see executor_b200.HybridB200Executor")
+
+    def finish_hybrid(self, handle) -> None:
+        pass
+
+    # ------------------------------------------------------------------ lifecycle hooks
+    def on_preempt(self, req) -> None:
+        pass  # generated ids are kept: the re-prefill rebuilds prompt + y1..y_{d-1}
+
+    def on_finish(self, req) -> None:
+        self._tokens_cache.pop(req.id, None)
+
+    def close(self) -> None:
+        # Graphs are dropped; green contexts live until process exit (torch
+        # still holds ExternalStream / event objects bound to them).
+        torch.cuda.synchronize()
+        for p in self._partitions.values():
+            p.graphs.clear()
