@@ -1,0 +1,366 @@
+"""Headline benchmark: RAPID-Serve on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--qps Q] [--duration S] [--decode-sms 72] [--model llama3.1-8b]
+
+Workload (BASELINE.json configs[1], "cfg 2"): Llama-3.1-8B bf16 (random-init
+weights of the real shapes; no checkpoints offline), one B200, static SM split
+(decode 72 SMs = 9x8, prefill 76 SMs: the green-context-granular 50/50),
+synthetic trace `synthesize(WorkloadSpec(qps=Q, duration_s=S, seed=42,
+mean_prompt_tokens=1024, mean_output_tokens=256, sigma=0))` served by the
+real-time RAPID engine (prefill and decode of different requests concurrently
+on disjoint SM partitions over one shared paged KV cache).
+
+A "step" is one decode iteration of the engine (one CUDA-graph replay over
+the current batch; prefill chunks run concurrently on the other partition).
+W untimed warm-up steps (at least; the window also waits for the first 25% of
+the trace so the batch is in steady state), then exactly K timed steps between
+CUDA events on the decode stream. value = output tokens delivered in those K
+steps / their device time (whole-job tokens/s; N ranks -> sum of tokens / max
+window time). The SLO check (pooled p99 ITL <= 50 ms over the run) decides
+whether the point is SLO-constrained. Inputs are larger than L2 (KV cache and
+weights, ~30 GB per step), so no extra flush is needed.
+
+N > 1 (torchrun): one independent replica per GPU ("replicas only"; the path
+shards by request, no data-path collective), each rank its own trace (seed
+42+rank); barrier + max-over-ranks of the window time via NCCL all_reduce.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SLO_ITL_US = 50_000
+PROMPT, OUTPUT = 1024, 256
+
+
+def _peaks() -> dict:
+    p = {"hbm_gbs": 6543.4, "bf16_tflops": 1643.1, "bf16_tflops_sustained": 1381.0, "_src": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p.update(json.load(fh))
+            p["_src"] = "measured"
+    except OSError:
+        pass
+    return p
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU restatement of the path (oracle port), same metric."""
+    if rank != 0:
+        return
+    from oracle.cpu_baseline import run_sample
+    from paper_2601_11822_b200.specs import ARCHS
+
+    arch = ARCHS[args.model]
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(max(1, args.ref_steps)):
+        vals.append(run_sample(arch, PROMPT, OUTPUT, batch=8, decode_steps=1, prefill_tokens=32))
+    wall = time.perf_counter() - t0
+    v = statistics.median(x["value"] for x in vals)
+    line = {
+        "impl": "reference", "metric": "SLO-constrained output tokens/s per GPU (p99 ITL<=SLO); p50 TTFT; p99 ITL",
+        "value": v, "unit": "output tokens/s", "n_gpus": world, "steps": len(vals), "warmup": 0,
+        "ms_per_step": wall / len(vals) * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"cfg2 {args.model} in {PROMPT}/out {OUTPUT} (bounded CPU sample)"},
+        "cpu_baseline": {"value": v, "unit": "output tokens/s", "cores": vals[0]["cores"], "kind": "port",
+                         "sample": vals[0]["sample"]},
+        "e2e": {"value": v, "unit": "output tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def time_decode_attention(runner, stream, B: int, ctx: int, iters: int = 20) -> dict:
+    """Live roofline probe of the dominant decode kernel on the decode partition:
+    CUDA events over `iters` launches at the run's mean (B, ctx)."""
+    import torch
+
+    from paper_2601_11822_b200 import ops
+
+    arch = runner.arch
+    nbps = (ctx + 15) // 16
+    B = max(1, min(B, runner.num_slots, runner.num_blocks // max(1, nbps)))
+    slots = torch.arange(B, dtype=torch.int32, device=runner.device)
+    seq = torch.full((B,), ctx, dtype=torch.int32, device=runner.device)
+    bt = torch.arange(B * nbps, dtype=torch.int32, device=runner.device).view(B, nbps)
+    tbl = runner.block_table.clone()
+    tbl[:B, :nbps] = bt
+    q = torch.randn(B, arch.q_heads, arch.head_dim, device=runner.device).bfloat16()
+    out = torch.empty_like(q)
+    splits = runner.decode_splits(B, ctx, 72)
+    cache = runner.kv[0]
+    sh = stream.cuda_stream
+    for _ in range(3):
+        ops.decode_attention(q, cache, tbl, slots, seq, out, num_kv_heads=arch.kv_heads, splits=splits,
+                             workspace=runner.attn_ws, stream=sh)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(iters):
+        ops.decode_attention(q, cache, tbl, slots, seq, out, num_kv_heads=arch.kv_heads, splits=splits,
+                             workspace=runner.attn_ws, stream=sh)
+    e1.record(stream)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    byts = B * ctx * arch.kv_heads * arch.head_dim * 2 * 2  # K+V bf16, one layer, one launch
+    return {"B": B, "ctx": ctx, "bytes": byts, "ms": ms, "gbs": byts / ms / 1e6}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=600)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--qps", type=float, default=24.0)
+    ap.add_argument("--duration", type=float, default=None)
+    ap.add_argument("--decode-sms", type=int, default=72)
+    ap.add_argument("--model", default="llama3.1-8b")
+    ap.add_argument("--ref-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    rank, world, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+
+    from paper_2601_11822_b200 import ops
+    from paper_2601_11822_b200.arm import CostParams
+    from paper_2601_11822_b200.clock import RealTimeLoop
+    from paper_2601_11822_b200.engines.rapid import RapidEngine
+    from paper_2601_11822_b200.executor_b200 import B200Executor
+    from paper_2601_11822_b200.harness import check_invariants
+    from paper_2601_11822_b200.slo import SloSpec, percentile_nearest_rank, summarize
+    from paper_2601_11822_b200.specs import ARCHS, AllocationDecision, AllocationMode, b200_spec
+    from paper_2601_11822_b200.traffic import WorkloadSpec, synthesize
+
+    torch.cuda.set_device(local)
+    arch = ARCHS[args.model]
+    peaks = _peaks()
+    # trace long enough for warm-up + K steps (~12 ms per step at steady state)
+    duration = args.duration or max(30.0, 8.0 + (args.warmup + args.steps) * 0.02 * 1.6)
+    items = synthesize(WorkloadSpec(qps=args.qps, duration_s=duration, seed=42 + rank, mean_prompt_tokens=PROMPT,
+                                    mean_output_tokens=OUTPUT, sigma=0.0))
+    ex = B200Executor(arch, seed=rank, static_decode_sms=args.decode_sms, max_batch=256, chunk_tokens=2048,
+                      max_context=PROMPT + OUTPUT + 64, num_slots=1024)
+    ex.warmup()
+    d_sms = ex._partitions[args.decode_sms].d_sms
+    p_sms = ex._partitions[args.decode_sms].p_sms
+    total = ex.total_sms
+    static = AllocationDecision(AllocationMode.PARTITION, p_sms / total, d_sms / total)
+    model = arch.model_spec()
+    slo = SloSpec(itl_slo_us=SLO_ITL_US)
+    engine = RapidEngine(model, b200_spec(), CostParams(), slo, chunk_tokens=2048, max_batch=256, executor=ex,
+                         static_decision=static)
+
+    # ---- timed window over decode steps, hooked on the executor
+    horizon = int(duration * 1e6)
+    win = {"start_handle": None, "end_handle": None, "tokens": 0, "steps": 0, "host0": None, "host1": None,
+           "h2d0": 0, "h2d1": 0, "d2h0": 0, "d2h1": 0, "launch0": 0, "launch1": 0, "Bs": [], "ctxs": []}
+    clocks = ClockSampler(local)
+    orig_launch = ex.launch_decode
+    orig_finish = ex.finish_decode
+    loop_ref = {}
+
+    def launch_decode(members, decision, co):
+        h = orig_launch(members, decision, co)
+        st = win
+        steady = loop_ref["loop"].clock_us() >= 0.25 * horizon
+        if st["start_handle"] is None and ex.decode_steps > args.warmup and steady:
+            st["start_handle"] = h
+            st["host0"] = time.perf_counter()
+            st["h2d0"], st["d2h0"], st["launch0"] = ex.h2d_bytes, ex.d2h_bytes, ex.gpu_launches
+            clocks.start()
+        if st["start_handle"] is not None and st["end_handle"] is None:
+            st["steps"] += 1
+            st["Bs"].append(len(members))
+            st["ctxs"].append(sum(r.context_tokens for r in members) / len(members))
+            h._win = True
+            if st["steps"] == args.steps:
+                st["end_handle"] = h
+        return h
+
+    def finish_decode(h):
+        orig_finish(h)
+        if getattr(h, "_win", False):
+            win["tokens"] += sum(1 for lame in h.lame if not lame)
+            if h is win["end_handle"]:
+                win["host1"] = time.perf_counter()
+                win["h2d1"], win["d2h1"], win["launch1"] = ex.h2d_bytes, ex.d2h_bytes, ex.gpu_launches
+                win["clocks"] = clocks.stop()
+
+    ex.launch_decode = launch_decode
+    ex.finish_decode = finish_decode
+
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    loop = RealTimeLoop(until_us=horizon)
+    loop_ref["loop"] = loop
+    engine.prime(loop, items)
+    t_run = time.perf_counter()
+    loop.run(engine.on_event)
+    t_run = time.perf_counter() - t_run
+    torch.cuda.synchronize()
+    check_invariants(engine)
+
+    complete = win["end_handle"] is not None and win["host1"] is not None
+    if complete:
+        ms = win["start_handle"].ev0.elapsed_time(win["end_handle"].ev1)
+        host_s = win["host1"] - win["host0"]
+    else:
+        ms, host_s = float("nan"), float("nan")
+    tokens = win["tokens"]
+    if world > 1:
+        t = torch.tensor([ms, host_s, tokens], dtype=torch.float64, device="cuda")
+        mx = t.clone()
+        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
+        sm = t.clone()
+        torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
+        ms, host_s, tokens = float(mx[0]), float(mx[1]), float(sm[2])
+    summ = summarize(engine.label, args.qps, engine.requests, slo, loop.horizon_us, engine.busy_intervals,
+                     engine.pools)
+    value = tokens / (ms / 1e3) if complete else 0.0
+    e2e_value = tokens / host_s if complete else 0.0
+
+    # live roofline probe of the dominant decode kernel (decode attention)
+    part = ex._partitions[args.decode_sms]
+    mB = int(round(statistics.mean(win["Bs"]))) if win["Bs"] else 64
+    mctx = int(round(statistics.mean(win["ctxs"]))) if win["ctxs"] else PROMPT + OUTPUT // 2
+    probe = time_decode_attention(ex.runner, part.ds, mB, mctx)
+    hbm = peaks["hbm_gbs"]
+    steps = max(1, win["steps"])
+    h2d = (win["h2d1"] - win["h2d0"]) / steps if complete else 0
+    d2h = (win["d2h1"] - win["d2h0"]) / steps if complete else 0
+    launches = int(win["launch1"] - win["launch0"]) if complete else 0
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle.cpu_baseline import run_sample
+
+        cpu = run_sample(arch, PROMPT, OUTPUT, batch=8, decode_steps=1, prefill_tokens=32)
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank != 0:
+        return
+    profile_path = os.path.join(ROOT, "profiles")
+    line = {
+        "metric": "SLO-constrained output tokens/s per GPU (p99 ITL<=SLO); p50 TTFT; p99 ITL",
+        "value": value,
+        "unit": "output tokens/s",
+        "n_gpus": world,
+        "steps": win["steps"],
+        "warmup": args.warmup,
+        "ms_per_step": ms / steps if complete else None,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (random-init Llama-3.1-8B weights, synthesize() trace)",
+        "config": {
+            "workload": f"cfg2: {args.model} bf16, 1x B200 per replica, static split decode {d_sms} / prefill "
+                        f"{p_sms} SMs, trace in {PROMPT}/out {OUTPUT} sigma=0 at {args.qps} QPS for {duration:.0f} s",
+            "qps_per_replica": args.qps,
+            "parallelism": f"replicas x{world}",
+            "l2": "inputs > L2 (KV + weights ~30 GB per step); no flush",
+            "step": "one decode iteration (CUDA-graph replay); prefill runs concurrently on its partition",
+        },
+        "p50_ttft_ms": summ.ttft_p50_us / 1e3,
+        "p99_itl_ms": summ.itl_p99_us / 1e3,
+        "p95_itl_ms": summ.itl_p95_us / 1e3,
+        "slo_itl_ms": SLO_ITL_US / 1e3,
+        "slo_met": bool(summ.itl_p99_us <= SLO_ITL_US),
+        "run_tokens_per_s": summ.tokens_per_s,
+        "goodput_req_s": summ.goodput,
+        "mean_decode_batch": statistics.mean(win["Bs"]) if win["Bs"] else None,
+        "mean_context": statistics.mean(win["ctxs"]) if win["ctxs"] else None,
+        "e2e": {"value": e2e_value, "unit": "output tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "note": "host wall clock over the same K steps through RapidEngine/B200Executor (pinned H2D of "
+                        "step inputs + block-table deltas + prefill ids, D2H of sampled ids, every step)"},
+        "roofline": {"kernel": "decode_attn_kernel (K3)", "bound": "hbm", "achieved": probe["gbs"], "peak": hbm,
+                     "unit": "GB/s", "frac": probe["gbs"] / hbm, "traffic": None,
+                     "per_launch": f"B={probe['B']} ctx={probe['ctx']}: {probe['bytes']} B (K+V bf16, 1 layer) "
+                                   f"in {probe['ms'] * 1e3:.1f} us on the {d_sms}-SM decode partition",
+                     "peak_src": peaks["_src"]},
+        "gpu_launches": launches,
+        "clocks": win.get("clocks", {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}),
+        "cpu_baseline": cpu,
+        "run_wall_s": t_run,
+        "requests": len(engine.requests),
+        "finished": sum(1 for r in engine.requests if r.state.value == "finished"),
+        "profiles": profile_path,
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -167,3 +167,39 @@ def paged_attention_ref(q, cache, block_row, n):
     G = q.shape[0] // Hkv
     s = torch.einsum("hd,nhd->hn", q.float(), k.repeat_interleave(G, 1)) / math.sqrt(D)
     return torch.einsum("hn,nhd->hd", torch.softmax(s, -1), v.repeat_interleave(G, 1))
+
+
+def decode_batch(orc: Oracle, ids: torch.Tensor, positions: list[int], kvs: list[list]) -> torch.Tensor:
+    """One batched decode step (weights read once for all rows; attention per
+    sequence over its own KV). kvs[b][layer] = (K [n,Hkv,D], V) is extended in place.
+    Returns logits [B, V]."""
+    a, s = orc.a, orc.s
+    B = ids.shape[0]
+    D = a.head_dim
+    G = a.q_heads // a.kv_heads
+    x = s["embed"][ids.long()]
+    pos = torch.tensor(positions)
+    for i in range(a.layers):
+        p = f"layers.{i}."
+        h = _rms(x, s[p + "ln1"], a.rms_eps)
+        q = h @ s[p + "q"].T
+        k = h @ s[p + "k"].T
+        v = h @ s[p + "v"].T
+        if a.qkv_bias:
+            q, k, v = q + s[p + "bq"], k + s[p + "bk"], v + s[p + "bv"]
+        q = _rope(q.view(B, a.q_heads, D), pos, orc.freqs)
+        k = _rope(k.view(B, a.kv_heads, D), pos, orc.freqs)
+        v = v.view(B, a.kv_heads, D)
+        o = torch.empty(B, a.q_heads, D)
+        for b in range(B):
+            K, V = kvs[b][i]
+            K = torch.cat([K, k[b : b + 1]], 0)
+            V = torch.cat([V, v[b : b + 1]], 0)
+            kvs[b][i] = (K, V)
+            sc = torch.einsum("hd,nhd->hn", q[b], K.repeat_interleave(G, 1)) / math.sqrt(D)
+            o[b] = torch.einsum("hn,nhd->hd", torch.softmax(sc, -1), V.repeat_interleave(G, 1))
+        x = x + o.reshape(B, -1) @ s[p + "o"].T
+        h = _rms(x, s[p + "ln2"], a.rms_eps)
+        x = x + (torch.nn.functional.silu(h @ s[p + "gate"].T) * (h @ s[p + "up"].T)) @ s[p + "down"].T
+    x = _rms(x, s["norm"], a.rms_eps)
+    return x @ s.get("lm_head", s["embed"]).T

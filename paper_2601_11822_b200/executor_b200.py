@@ -38,9 +38,6 @@ MAX_UPDATES = 1 << 16
 
 
 class GpuHandle:
-    __slots__ = ("kind", "ev0", "ev1", "gpu_us", "cu_fraction", "members", "start_us", "lame", "rows", "launch_ns",
-                 "req", "last_chunk")
-
     def __init__(self, kind, stream, cu_fraction):
         self.kind = kind
         self.ev0 = torch.cuda.Event(enable_timing=True)
