@@ -136,7 +136,7 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def time_decode_attention(runner, stream, B: int, ctx: int, iters: int = 20) -> dict:
+def time_decode_attention(runner, stream, B: int, ctx: int, sms: int, iters: int = 20) -> dict:
     """Live roofline probe of the dominant decode kernel on the decode partition:
     CUDA events over `iters` launches at the run's mean (B, ctx)."""
     import torch
@@ -153,17 +153,16 @@ def time_decode_attention(runner, stream, B: int, ctx: int, iters: int = 20) -> 
     tbl[:B, :nbps] = bt
     q = torch.randn(B, arch.q_heads, arch.head_dim, device=runner.device).bfloat16()
     out = torch.empty_like(q)
-    splits = runner.decode_splits(B, ctx, 72)
     cache = runner.kv[0]
     sh = stream.cuda_stream
     for _ in range(3):
-        ops.decode_attention(q, cache, tbl, slots, seq, out, num_kv_heads=arch.kv_heads, splits=splits,
-                             workspace=runner.attn_ws, stream=sh)
+        ops.decode_attention(q, cache, tbl, slots, seq, out, num_kv_heads=arch.kv_heads, max_pages=nbps,
+                             workspace=runner.attn_ws, num_sms=sms, stream=sh)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(iters):
-        ops.decode_attention(q, cache, tbl, slots, seq, out, num_kv_heads=arch.kv_heads, splits=splits,
-                             workspace=runner.attn_ws, stream=sh)
+        ops.decode_attention(q, cache, tbl, slots, seq, out, num_kv_heads=arch.kv_heads, max_pages=nbps,
+                             workspace=runner.attn_ws, num_sms=sms, stream=sh)
     e1.record(stream)
     e1.synchronize()
     ms = e0.elapsed_time(e1) / iters
@@ -296,7 +295,7 @@ def main():
     part = ex._partitions[args.decode_sms]
     mB = int(round(statistics.mean(win["Bs"]))) if win["Bs"] else 64
     mctx = int(round(statistics.mean(win["ctxs"]))) if win["ctxs"] else PROMPT + OUTPUT // 2
-    probe = time_decode_attention(ex.runner, part.ds, mB, mctx)
+    probe = time_decode_attention(ex.runner, part.ds, mB, mctx, part.d_sms)
     hbm = peaks["hbm_gbs"]
     steps = max(1, win["steps"])
     h2d = (win["h2d1"] - win["h2d0"]) / steps if complete else 0

@@ -50,12 +50,15 @@ int rb_gemm_bf16(const void* X, const void* W, void* Y, const void* bias, const 
  *   out[b,h,:] = softmax(scale * q[b,h,:] . K[slot_b, :seq_lens[b]]) V
  * Replaces the KV-read term kv_cache_bytes(model, total_kv_tokens) of
  * decode_time (costmodel.py:131). row_slot[b] selects the block-table row;
- * rows with seq_lens[b] <= 0 are skipped (graph padding). splits > 1 needs
- * workspace of B*Hq*splits*(head_dim+2)*4 bytes. */
+ * rows with seq_lens[b] <= 0 are skipped (graph padding). max_pages bounds
+ * ceil(seq_lens[b]/16) over the launch (sequences are cut into 16-page work
+ * items); when max_pages > 16 the workspace must hold
+ * B*Hq*ceil(max_pages/16)*(head_dim+2)*4 bytes. num_blocks = pages in the
+ * cache layer (TMA extent); num_sms = SMs of the launching partition. */
 int rb_decode_attention(const void* q, long long q_tok_stride, const void* cache_layer, const int* block_table,
                         int bt_stride, const int* row_slot, const int* seq_lens, void* out,
                         long long out_tok_stride, void* workspace, size_t ws_bytes, int B, int Hq, int Hkv,
-                        int head_dim, int splits, float scale, void* stream);
+                        int head_dim, int max_pages, float scale, int num_blocks, int num_sms, void* stream);
 
 /* K2 — causal prefill attention of one chunk (positions start..start+T-1)
  * against the paged cache [0, start+T). Replaces the attention share of

@@ -1,21 +1,27 @@
-// K3: decode paged attention (HBM-bound).
+// K3: decode paged attention (HBM-bound), tensor-core + TMA version.
 //
 // Realizes the KV-read term kv_cache_bytes(model, total_kv_tokens) of
 // decode_time (reference pkg/src/pdsim/costmodel.py:129-133).
 //
-// Cache layout (one layer): [num_blocks][2 (K,V)][Hkv][16 tokens][D] bf16, so
-// the K (or V) page of one kv-head is a contiguous 4 KB run that one
-// cp.async.bulk moves into shared memory. Grid = (Hkv, B, splits); each CTA
-// serves all G = Hq/Hkv query heads of one kv head (GQA) over one split of
-// the sequence's pages. Each of the 4 warps owns a private STAGES-deep smem
-// ring fed by bulk copies (lane 0 issues, mbarrier completes), so the warp
-// keeps STAGES x 8 KB in flight without spending registers on it.
+// Cache layout (one layer): [num_blocks][2 (K,V)][Hkv][16 tokens][D=128] bf16,
+// viewed by TMA as a 2D tensor of 256-byte rows; one page of one kv-head is 16
+// consecutive rows. Each page half (64 dims) is fetched by one
+// cp.async.bulk.tensor box {64, 16} with the 128B swizzle, so every ldmatrix
+// below is bank-conflict free.
 //
-// Lane mapping inside a page: lane = 8*grp + c; grp (0..3) owns tokens
-// 4*grp..4*grp+3, c (0..7) owns dims {8c..8c+7} U {64+8c..64+8c+7}. q.k
-// partials reduce over the 8 lanes of a group (3 shuffles); every group keeps
-// its own online-softmax state, merged once at the end (no per-page
-// cross-group traffic).
+// Work decomposition: item = (sequence b, kv head h, chunk c of 16 pages).
+// Persistent grid; every warp owns a private STAGES-deep smem ring and streams
+// the pages of its items (item = global_warp, +num_warps, ...) back to back:
+// lane 0 keeps STAGES pages in flight across item boundaries.
+//
+// Math per page (transposed so GQA padding is free):
+//   S^T[16 tok x 8 heads] = K[16 x 128] . Q^T[128 x 8]   (8 x mma.m16n8k16)
+//   online softmax per head (column) over tokens
+//   O^T[128 x 8] += V^T[128 x 16] . P^T[16 x 8]           (8 x mma.m16n8k16)
+// P^T goes accumulator -> bf16 -> 256 B smem -> ldmatrix.trans (B operand).
+// Items of multi-chunk sequences write fp32 partials (m, l, O) that a combine
+// kernel merges; single-chunk sequences write the output directly.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <cfloat>
@@ -24,342 +30,353 @@
 
 namespace rb {
 
-constexpr int kDecD = 128;
+constexpr int kD = 128;
 constexpr int kPage = 16;
-constexpr int kDecWarps = 4;
-constexpr int kDecStages = 3;
-constexpr int kPageBytes = kPage * kDecD * 2;  // 4 KB
+constexpr int kChunkPages = 16;           // pages per work item (256 tokens)
+constexpr int kWarps = 8;
+constexpr int kStages = 3;
+constexpr int kStageBytes = 4 * 2048;     // K lo/hi + V lo/hi, 16 rows x 128 B each
+constexpr int kPStageBytes = 256;         // P^T staging per warp
 
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x2_t(uint32_t addr, uint32_t& r0, uint32_t& r1) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(kEvictFirst)
-      : "memory");
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-template <int G>
-__global__ void __launch_bounds__(kDecWarps * 32)
-    decode_attn_kernel(const __nv_bfloat16* __restrict__ q, long long q_tok_stride,
-                       const __nv_bfloat16* __restrict__ cache, const int* __restrict__ block_table, int bt_stride,
-                       const int* __restrict__ row_slot, const int* __restrict__ seq_lens,
-                       __nv_bfloat16* __restrict__ out, long long out_tok_stride, float* __restrict__ part_o,
-                       float* __restrict__ part_ml, int Hkv, int splits, float scale_log2) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t* ring = smem;  // [warps][stages][8 KB]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kDecWarps * kDecStages * 2 * kPageBytes);
+// byte offset of 16-byte chunk `ch` (0..15 over 128 dims) of token row `r` in a staged page half-pair
+__device__ __forceinline__ uint32_t pg_off(int r, int ch) {
+  return (uint32_t)((ch >> 3) * 2048 + r * 128 + (((ch & 7) ^ (r & 7)) << 4));
+}
 
-  const int h = blockIdx.x;
-  const int b = blockIdx.y;
-  const int s = blockIdx.z;
-  const int Hq = Hkv * G;
+struct DecArgs {
+  const __nv_bfloat16* q;
+  long long q_tok_stride;
+  const int* block_table;
+  int bt_stride;
+  const int* row_slot;
+  const int* seq_lens;
+  __nv_bfloat16* out;
+  long long out_tok_stride;
+  float* part_o;   // [items][G][128]
+  float* part_ml;  // [items][G][2]
+  int B, Hkv, G, splits;
+  float scale_log2;
+};
+
+// decode an item index -> (b, h, chunk); returns pages [p0, p1) (empty if past the sequence)
+__device__ __forceinline__ void item_pages(const DecArgs& a, int item, int& b, int& h, int& c, int& p0, int& p1,
+                                           int& n) {
+  c = item % a.splits;
+  const int bh = item / a.splits;
+  h = bh % a.Hkv;
+  b = bh / a.Hkv;
+  n = a.seq_lens[b];
+  const int nb = (n + kPage - 1) / kPage;
+  p0 = c * kChunkPages;
+  p1 = min(nb, p0 + kChunkPages);
+}
+
+__global__ void __launch_bounds__(kWarps * 32, 1)
+    decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map, const DecArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int n = seq_lens[b];
-  const int nb = (n + kPage - 1) / kPage;
-  const int per = (nb + splits - 1) / max(splits, 1);
-  const int j0 = s * per;
-  const int j1 = min(nb, j0 + per);
-
-  if (n <= 0 || j0 >= j1) {
-    // empty split (or padded row): publish a neutral partial
-    if (splits > 1 && threadIdx.x < G) {
-      const size_t idx = ((size_t)b * Hq + h * G + threadIdx.x) * splits + s;
-      part_ml[2 * idx] = -FLT_MAX;
-      part_ml[2 * idx + 1] = 0.f;
-    }
-    return;
-  }
-  const int* bt = block_table + (size_t)row_slot[b] * bt_stride;
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kDecWarps * kDecStages; ++i) mbar_init(&bars[i], 1);
-    fence_barrier_init();
-  }
-  __syncthreads();
-
-  // blocks of this warp: j0 + warp + 4*i
-  const int my_first = j0 + warp;
-  const int cnt = (my_first < j1) ? (j1 - my_first + kDecWarps - 1) / kDecWarps : 0;
-  uint8_t* my_ring = ring + (size_t)warp * kDecStages * 2 * kPageBytes;
-  uint64_t* my_bars = bars + warp * kDecStages;
-  const size_t head_off = (size_t)h * kPage * kDecD;                // within K or V half
-  const size_t half_stride = (size_t)Hkv * kPage * kDecD;           // K -> V
-  const size_t page_stride = 2 * half_stride;
-
+  uint8_t* ring = smem + (size_t)warp * kStages * kStageBytes;
+  uint8_t* pst = smem + (size_t)kWarps * kStages * kStageBytes + warp * kPStageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kWarps * kStages * kStageBytes +
+                                               kWarps * kPStageBytes) + warp * kStages;
   if (lane == 0) {
-    for (int i = 0; i < kDecStages && i < cnt; ++i) {
-      const int page = bt[my_first + i * kDecWarps];
-      const __nv_bfloat16* kp = cache + (size_t)page * page_stride + head_off;
-      mbar_arrive_expect_tx(&my_bars[i], 2 * kPageBytes);
-      bulk_g2s(my_ring + (size_t)i * 2 * kPageBytes, kp, kPageBytes, &my_bars[i]);
-      bulk_g2s(my_ring + (size_t)i * 2 * kPageBytes + kPageBytes, kp + half_stride, kPageBytes, &my_bars[i]);
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&kv_map);
+  }
+  __syncwarp();
+
+  const int total_items = a.B * a.Hkv * a.splits;
+  const int gw = blockIdx.x * kWarps + warp;
+  const int nw = gridDim.x * kWarps;
+  const int g = lane >> 2;  // group id (row of the fragment)
+  const int t = lane & 3;
+
+  // ---------------- producer cursor (lane 0): next page to fetch
+  int pi = gw, pp = 0, pp1 = 0, pb = 0, ph = 0, pc = 0, pn = 0;
+  auto p_seek = [&]() {  // advance pi to an item with pages; sets pp..pp1
+    while (pi < total_items) {
+      item_pages(a, pi, pb, ph, pc, pp, pp1, pn);
+      if (pp < pp1) return;
+      pi += nw;
+    }
+  };
+  int issued = 0;
+  auto p_issue = [&](int stage) {
+    const int slot = a.row_slot[pb];
+    const int page = a.block_table[(size_t)slot * a.bt_stride + pp];
+    const int rowK = ((page * 2 + 0) * a.Hkv + ph) * kPage;
+    const int rowV = ((page * 2 + 1) * a.Hkv + ph) * kPage;
+    uint8_t* dst = ring + (size_t)stage * kStageBytes;
+    mbar_arrive_expect_tx(&bars[stage], kStageBytes);
+    tma_load_2d(dst, &kv_map, &bars[stage], 0, rowK, kEvictFirst);
+    tma_load_2d(dst + 2048, &kv_map, &bars[stage], 64, rowK, kEvictFirst);
+    tma_load_2d(dst + 4096, &kv_map, &bars[stage], 0, rowV, kEvictFirst);
+    tma_load_2d(dst + 6144, &kv_map, &bars[stage], 64, rowV, kEvictFirst);
+    if (++pp == pp1) {
+      pi += nw;
+      p_seek();
+    }
+  };
+  if (lane == 0) {
+    p_seek();
+    for (int s = 0; s < kStages && pi < total_items; ++s) {
+      p_issue(s);
+      ++issued;
     }
   }
 
-  const int grp = lane >> 3;
-  const int c = lane & 7;
-  // q fragment: dims 8c..8c+7 and 64+8c..64+8c+7 for every head of the group
-  float qf[G][16];
-  const __nv_bfloat16* qb = q + (size_t)b * q_tok_stride + (size_t)h * G * kDecD;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int item = gw; item < total_items; item += nw) {
+    int b, h, c, p0, p1, n;
+    item_pages(a, item, b, h, c, p0, p1, n);
+    if (p0 >= p1) continue;
+    // Q^T fragments (B operand): b0 = (dims 16kk+2t.., head g), b1 = (dims 16kk+8+2t.., head g)
+    uint32_t qb[8][2];
+    {
+      const __nv_bfloat16* qrow = a.q + (size_t)b * a.q_tok_stride + (size_t)(h * a.G + g) * kD;
+      const bool hv = g < a.G;
 #pragma unroll
-  for (int g = 0; g < G; ++g) {
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      uint4 u = *reinterpret_cast<const uint4*>(qb + g * kDecD + hh * 64 + 8 * c);
-      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float2 f = unpack_bf16x2(w[j]);
-        qf[g][hh * 8 + 2 * j] = f.x * scale_log2;
-        qf[g][hh * 8 + 2 * j + 1] = f.y * scale_log2;
+      for (int kk = 0; kk < 8; ++kk) {
+        qb[kk][0] = hv ? *reinterpret_cast<const uint32_t*>(qrow + 16 * kk + 2 * t) : 0u;
+        qb[kk][1] = hv ? *reinterpret_cast<const uint32_t*>(qrow + 16 * kk + 8 + 2 * t) : 0u;
       }
     }
-  }
-  float m_run[G], l_run[G], acc[G][16];
+    float o[8][4];
 #pragma unroll
-  for (int g = 0; g < G; ++g) {
-    m_run[g] = -FLT_MAX;
-    l_run[g] = 0.f;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) acc[g][j] = 0.f;
-  }
+    for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    float m0 = -FLT_MAX, m1 = -FLT_MAX;  // running max for heads 2t, 2t+1
+    float l0 = 0.f, l1 = 0.f;            // per-thread partial sums (tokens g, g+8)
 
-  for (int i = 0; i < cnt; ++i) {
-    const int stage = i % kDecStages;
-    const uint32_t parity = (uint32_t)((i / kDecStages) & 1);
-    mbar_wait(&my_bars[stage], parity);
-    const uint8_t* kbuf = my_ring + (size_t)stage * 2 * kPageBytes;
-    const uint8_t* vbuf = kbuf + kPageBytes;
-    const int jpage = my_first + i * kDecWarps;
-    float sc[G][4];
+    for (int p = p0; p < p1; ++p) {
+      mbar_wait(&bars[stage], phase);
+      const uint32_t base = smem_u32(ring + (size_t)stage * kStageBytes);
+      // ---- S^T = K Q^T
+      float s[4] = {0.f, 0.f, 0.f, 0.f};
+      const int mi = lane >> 3;
+      const int rr = (mi & 1) * 8 + (lane & 7);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int t = grp * 4 + u;
-      const uint4 k0 = *reinterpret_cast<const uint4*>(kbuf + t * 256 + 16 * c);
-      const uint4 k1 = *reinterpret_cast<const uint4*>(kbuf + t * 256 + 128 + 16 * c);
-      const uint32_t kw[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
-      float kf[16];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        float2 f = unpack_bf16x2(kw[j]);
-        kf[2 * j] = f.x;
-        kf[2 * j + 1] = f.y;
+      for (int kk = 0; kk < 8; ++kk) {
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4(base + pg_off(rr, 2 * kk + (mi >> 1)), a0, a1, a2, a3);
+        mma_bf16_16816(s, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
       }
+      // ---- mask + online softmax (columns = heads 2t, 2t+1; rows = tokens g, g+8)
+      const int tok0 = p * kPage + g;
+      float s00 = s[0] * a.scale_log2, s01 = s[1] * a.scale_log2;
+      float s10 = s[2] * a.scale_log2, s11 = s[3] * a.scale_log2;
+      if (tok0 >= n) { s00 = -FLT_MAX; s01 = -FLT_MAX; }
+      if (tok0 + 8 >= n) { s10 = -FLT_MAX; s11 = -FLT_MAX; }
+      float mx0 = fmaxf(s00, s10), mx1 = fmaxf(s01, s11);
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        float a = 0.f;
-#pragma unroll
-        for (int j = 0; j < 16; ++j) a = fmaf(qf[g][j], kf[j], a);
-        sc[g][u] = a;
+      for (int off = 4; off <= 16; off <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
       }
+      const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+      const float al0 = exp2f(m0 - mn0), al1 = exp2f(m1 - mn1);  // m0=-FLT_MAX first: exp2(-huge)=0
+      m0 = mn0;
+      m1 = mn1;
+      const float p00 = (s00 == -FLT_MAX) ? 0.f : exp2f(s00 - mn0);
+      const float p01 = (s01 == -FLT_MAX) ? 0.f : exp2f(s01 - mn1);
+      const float p10 = (s10 == -FLT_MAX) ? 0.f : exp2f(s10 - mn0);
+      const float p11 = (s11 == -FLT_MAX) ? 0.f : exp2f(s11 - mn1);
+      l0 = l0 * al0 + p00 + p10;
+      l1 = l1 * al1 + p01 + p11;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        o[i][0] *= al0;
+        o[i][1] *= al1;
+        o[i][2] *= al0;
+        o[i][3] *= al1;
+      }
+      // ---- rows past the sequence end in the last page hold stale (possibly non-finite)
+      // V; P is 0 there but 0 * NaN would still poison the MMA, so zero those rows.
+      const int valid = n - p * kPage;
+      if (valid < kPage) {
+        for (int i = lane; i < (kPage - valid) * 16; i += 32) {
+          const int r = valid + (i >> 4);
+          asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(base + 4096 + pg_off(r, i & 15)), "r"(0u)
+                       : "memory");
+        }
+      }
+      // ---- P^T -> smem [16 tok][8 heads] bf16 -> B fragments
+      uint32_t* pw = reinterpret_cast<uint32_t*>(pst);
+      pw[g * 4 + t] = pack_bf16x2(p00, p01);
+      pw[(g + 8) * 4 + t] = pack_bf16x2(p10, p11);
+      __syncwarp();
+      uint32_t pb0, pb1;
+      ldsm_x2_t(smem_u32(pst) + (lane & 15) * 16, pb0, pb1);
+      // ---- O^T += V^T P^T over 8 m-tiles of 16 dims
+      const int vr = (mi >> 1) * 8 + (lane & 7);
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4_t(base + 4096 + pg_off(vr, 2 * mt + (mi & 1)), a0, a1, a2, a3);
+        mma_bf16_16816(o[mt], a0, a1, a2, a3, pb0, pb1);
+      }
+      __syncwarp();  // every lane done with this stage and with pst
+      if (lane == 0 && pi < total_items) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        p_issue(stage);
+      }
+      if (++stage == kStages) { stage = 0; phase ^= 1; }
     }
+    // ---- finalize item: reduce l over the 8 row groups
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        float a = sc[g][u];
-        a += __shfl_xor_sync(0xffffffffu, a, 1);
-        a += __shfl_xor_sync(0xffffffffu, a, 2);
-        a += __shfl_xor_sync(0xffffffffu, a, 4);
-        const int pos = jpage * kPage + grp * 4 + u;
-        sc[g][u] = (pos < n) ? a : -FLT_MAX;
-      }
+    for (int off = 4; off <= 16; off <<= 1) {
+      l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, off);
     }
-    float vf[4][16];
+    const int nchunks = ((n + kPage - 1) / kPage + kChunkPages - 1) / kChunkPages;
+    const int hd0 = 2 * t, hd1 = 2 * t + 1;
+    if (nchunks == 1) {
+      const float i0 = l0 > 0.f ? 1.f / l0 : 0.f, i1 = l1 > 0.f ? 1.f / l1 : 0.f;
+      __nv_bfloat16* ob = a.out + (size_t)b * a.out_tok_stride + (size_t)h * a.G * kD;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int t = grp * 4 + u;
-      const uint4 v0 = *reinterpret_cast<const uint4*>(vbuf + t * 256 + 16 * c);
-      const uint4 v1 = *reinterpret_cast<const uint4*>(vbuf + t * 256 + 128 + 16 * c);
-      const uint32_t vw[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-      const bool ok = (jpage * kPage + t) < n;  // stale cache rows may hold NaN bit patterns
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        float2 f = unpack_bf16x2(vw[j]);
-        vf[u][2 * j] = ok ? f.x : 0.f;
-        vf[u][2 * j + 1] = ok ? f.y : 0.f;
+      for (int mt = 0; mt < 8; ++mt) {
+        const int d0 = mt * 16 + g;
+        if (hd0 < a.G) {
+          ob[(size_t)hd0 * kD + d0] = __float2bfloat16_rn(o[mt][0] * i0);
+          ob[(size_t)hd0 * kD + d0 + 8] = __float2bfloat16_rn(o[mt][2] * i0);
+        }
+        if (hd1 < a.G) {
+          ob[(size_t)hd1 * kD + d0] = __float2bfloat16_rn(o[mt][1] * i1);
+          ob[(size_t)hd1 * kD + d0 + 8] = __float2bfloat16_rn(o[mt][3] * i1);
+        }
       }
-    }
-    // all lanes are done with this stage's smem: refill it
-    __syncwarp();
-    if (lane == 0 && i + kDecStages < cnt) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      const int page = bt[my_first + (i + kDecStages) * kDecWarps];
-      const __nv_bfloat16* kp = cache + (size_t)page * page_stride + head_off;
-      mbar_arrive_expect_tx(&my_bars[stage], 2 * kPageBytes);
-      bulk_g2s(my_ring + (size_t)stage * 2 * kPageBytes, kp, kPageBytes, &my_bars[stage]);
-      bulk_g2s(my_ring + (size_t)stage * 2 * kPageBytes + kPageBytes, kp + half_stride, kPageBytes,
-               &my_bars[stage]);
-    }
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      float mx = fmaxf(fmaxf(sc[g][0], sc[g][1]), fmaxf(sc[g][2], sc[g][3]));
-      const float m_new = fmaxf(m_run[g], mx);
-      if (m_new == -FLT_MAX) continue;  // nothing valid yet for this group
-      const float alpha = exp2f(m_run[g] - m_new);
-      float p[4];
-      float ps = 0.f;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        p[u] = (sc[g][u] == -FLT_MAX) ? 0.f : exp2f(sc[g][u] - m_new);
-        ps += p[u];
-      }
-      l_run[g] = l_run[g] * alpha + ps;
-      m_run[g] = m_new;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        float a = acc[g][j] * alpha;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) a = fmaf(p[u], vf[u][j], a);
-        acc[g][j] = a;
-      }
-    }
-  }
-
-  // merge the 4 token groups of this warp (lanes c, c+8, c+16, c+24)
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-#pragma unroll
-    for (int off = 8; off <= 16; off <<= 1) {
-      const float mo = __shfl_xor_sync(0xffffffffu, m_run[g], off);
-      const float lo = __shfl_xor_sync(0xffffffffu, l_run[g], off);
-      const float mn = fmaxf(m_run[g], mo);
-      const float a_self = (m_run[g] == -FLT_MAX) ? 0.f : exp2f(m_run[g] - mn);
-      const float a_oth = (mo == -FLT_MAX) ? 0.f : exp2f(mo - mn);
-      l_run[g] = l_run[g] * a_self + lo * a_oth;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const float ao = __shfl_xor_sync(0xffffffffu, acc[g][j], off);
-        acc[g][j] = acc[g][j] * a_self + ao * a_oth;
-      }
-      m_run[g] = mn;
-    }
-  }
-  // publish per-warp partials [g][m, l, D] into this warp's (now idle) ring:
-  // every bulk copy the warp issued has been waited on inside the loop.
-  const int mstride = 2 + kDecD;
-  const size_t ring_floats = (size_t)kDecStages * 2 * kPageBytes / 4;
-  float* merge = reinterpret_cast<float*>(ring);
-  if (grp == 0) {
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      float* dst = merge + (size_t)warp * ring_floats + (size_t)g * mstride;
-      if (c == 0) {
-        dst[0] = m_run[g];
-        dst[1] = l_run[g];
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        dst[2 + 8 * c + j] = acc[g][j];
-        dst[2 + 64 + 8 * c + j] = acc[g][8 + j];
-      }
-    }
-  }
-  __syncthreads();
-  // final merge across warps: thread -> (g, d) pairs
-  for (int idx = threadIdx.x; idx < G * kDecD; idx += blockDim.x) {
-    const int g = idx / kDecD;
-    const int d = idx % kDecD;
-    float mx = -FLT_MAX;
-#pragma unroll
-    for (int w = 0; w < kDecWarps; ++w) mx = fmaxf(mx, merge[(size_t)w * ring_floats + (size_t)g * mstride]);
-    float l = 0.f, o = 0.f;
-#pragma unroll
-    for (int w = 0; w < kDecWarps; ++w) {
-      const float* src = merge + (size_t)w * ring_floats + (size_t)g * mstride;
-      const float a = (src[0] == -FLT_MAX) ? 0.f : exp2f(src[0] - mx);
-      l += src[1] * a;
-      o += src[2 + d] * a;
-    }
-    const int hq = h * G + g;
-    if (splits == 1) {
-      out[(size_t)b * out_tok_stride + (size_t)hq * kDecD + d] = __float2bfloat16_rn(l > 0.f ? o / l : 0.f);
     } else {
-      const size_t pidx = ((size_t)b * Hq + hq) * splits + s;
-      part_o[pidx * kDecD + d] = (l > 0.f) ? o / l : 0.f;
-      if (d == 0) {
-        part_ml[2 * pidx] = mx;
-        part_ml[2 * pidx + 1] = l;
+      const size_t pbase = (size_t)item * a.G;
+      const float i0 = l0 > 0.f ? 1.f / l0 : 0.f, i1 = l1 > 0.f ? 1.f / l1 : 0.f;
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        const int d0 = mt * 16 + g;
+        if (hd0 < a.G) {
+          a.part_o[(pbase + hd0) * kD + d0] = o[mt][0] * i0;
+          a.part_o[(pbase + hd0) * kD + d0 + 8] = o[mt][2] * i0;
+        }
+        if (hd1 < a.G) {
+          a.part_o[(pbase + hd1) * kD + d0] = o[mt][1] * i1;
+          a.part_o[(pbase + hd1) * kD + d0 + 8] = o[mt][3] * i1;
+        }
+      }
+      if (g == 0) {
+        if (hd0 < a.G) { a.part_ml[(pbase + hd0) * 2] = m0; a.part_ml[(pbase + hd0) * 2 + 1] = l0; }
+        if (hd1 < a.G) { a.part_ml[(pbase + hd1) * 2] = m1; a.part_ml[(pbase + hd1) * 2 + 1] = l1; }
       }
     }
   }
 }
 
+// merges the chunk partials of multi-chunk sequences; grid (B, Hq), 128 threads
 __global__ void decode_attn_combine_kernel(const float* __restrict__ part_o, const float* __restrict__ part_ml,
                                            const int* __restrict__ seq_lens, __nv_bfloat16* __restrict__ out,
-                                           long long out_tok_stride, int Hq, int splits) {
+                                           long long out_tok_stride, int Hkv, int G, int splits) {
   const int b = blockIdx.x;
   const int hq = blockIdx.y;
   const int d = threadIdx.x;
-  if (seq_lens[b] <= 0) return;
-  const size_t base = ((size_t)b * Hq + hq) * splits;
+  const int n = seq_lens[b];
+  const int nchunks = ((n + kPage - 1) / kPage + kChunkPages - 1) / kChunkPages;
+  if (n <= 0 || nchunks <= 1) return;
+  const int h = hq / G, hd = hq % G;
   float mx = -FLT_MAX;
-  for (int s = 0; s < splits; ++s)
-    if (part_ml[2 * (base + s) + 1] > 0.f) mx = fmaxf(mx, part_ml[2 * (base + s)]);
+  for (int c = 0; c < nchunks; ++c) {
+    const size_t it = ((size_t)(b * Hkv + h) * splits + c) * G + hd;
+    if (part_ml[it * 2 + 1] > 0.f) mx = fmaxf(mx, part_ml[it * 2]);
+  }
   float l = 0.f, o = 0.f;
-  for (int s = 0; s < splits; ++s) {
-    const float ls = part_ml[2 * (base + s) + 1];
-    if (ls <= 0.f) continue;
-    const float a = exp2f(part_ml[2 * (base + s)] - mx) * ls;
-    l += a;
-    o += a * part_o[(base + s) * kDecD + d];
+  for (int c = 0; c < nchunks; ++c) {
+    const size_t it = ((size_t)(b * Hkv + h) * splits + c) * G + hd;
+    const float lc = part_ml[it * 2 + 1];
+    if (lc <= 0.f) continue;
+    const float w = exp2f(part_ml[it * 2] - mx) * lc;
+    l += w;
+    o += w * part_o[it * kD + d];
   }
-  out[(size_t)b * out_tok_stride + (size_t)hq * kDecD + d] = __float2bfloat16_rn(l > 0.f ? o / l : 0.f);
-}
-
-template <int G>
-static int launch_decode(const void* q, long long qs, const void* cache, const int* bt, int bt_stride,
-                         const int* row_slot, const int* seq_lens, void* out, long long os, float* part_o,
-                         float* part_ml, int B, int Hkv, int splits, float scale_log2, cudaStream_t st) {
-  const int smem = kDecWarps * kDecStages * 2 * kPageBytes + kDecWarps * kDecStages * 8;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return set_cuda_error("decode attn smem attr", e);
-    attr = true;
-  }
-  dim3 grid(Hkv, B, splits);
-  decode_attn_kernel<G><<<grid, kDecWarps * 32, smem, st>>>(
-      (const __nv_bfloat16*)q, qs, (const __nv_bfloat16*)cache, bt, bt_stride, row_slot, seq_lens,
-      (__nv_bfloat16*)out, os, part_o, part_ml, Hkv, splits, scale_log2);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return set_cuda_error("decode attn launch", e);
-  if (splits > 1) {
-    decode_attn_combine_kernel<<<dim3(B, Hkv * G), kDecD, 0, st>>>(part_o, part_ml, seq_lens,
-                                                                   (__nv_bfloat16*)out, os, Hkv * G, splits);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return set_cuda_error("decode combine launch", e);
-  }
-  return 0;
+  out[(size_t)b * out_tok_stride + (size_t)hq * kD + d] = __float2bfloat16_rn(l > 0.f ? o / l : 0.f);
 }
 
 int decode_attention_launch(const void* q, long long q_tok_stride, const void* cache_layer, const int* block_table,
                             int bt_stride, const int* row_slot, const int* seq_lens, void* out,
                             long long out_tok_stride, void* workspace, size_t ws_bytes, int B, int Hq, int Hkv,
-                            int head_dim, int splits, float scale, cudaStream_t st) {
+                            int head_dim, int max_pages, float scale, int num_blocks, int num_sms, cudaStream_t st) {
   if (B <= 0) return 0;
-  if (head_dim != kDecD) return set_error("decode attention: head_dim must be 128");
+  if (head_dim != kD) return set_error("decode attention: head_dim must be 128");
   if (Hkv <= 0 || Hq % Hkv != 0) return set_error("decode attention: Hq must be a multiple of Hkv");
-  if (splits < 1) splits = 1;
-  float* part_o = nullptr;
-  float* part_ml = nullptr;
-  if (splits > 1) {
-    const size_t need = (size_t)B * Hq * splits * (kDecD + 2) * sizeof(float);
-    if (workspace == nullptr || ws_bytes < need) return set_error("decode attention: workspace too small");
-    part_o = reinterpret_cast<float*>(workspace);
-    part_ml = part_o + (size_t)B * Hq * splits * kDecD;
-  }
-  const float sl2 = scale * 1.4426950408889634f;
   const int G = Hq / Hkv;
-  switch (G) {
-    case 1: return launch_decode<1>(q, q_tok_stride, cache_layer, block_table, bt_stride, row_slot, seq_lens, out, out_tok_stride, part_o, part_ml, B, Hkv, splits, sl2, st);
-    case 2: return launch_decode<2>(q, q_tok_stride, cache_layer, block_table, bt_stride, row_slot, seq_lens, out, out_tok_stride, part_o, part_ml, B, Hkv, splits, sl2, st);
-    case 4: return launch_decode<4>(q, q_tok_stride, cache_layer, block_table, bt_stride, row_slot, seq_lens, out, out_tok_stride, part_o, part_ml, B, Hkv, splits, sl2, st);
-    case 5: return launch_decode<5>(q, q_tok_stride, cache_layer, block_table, bt_stride, row_slot, seq_lens, out, out_tok_stride, part_o, part_ml, B, Hkv, splits, sl2, st);
-    case 8: return launch_decode<8>(q, q_tok_stride, cache_layer, block_table, bt_stride, row_slot, seq_lens, out, out_tok_stride, part_o, part_ml, B, Hkv, splits, sl2, st);
-    default: return set_error("decode attention: unsupported GQA group size");
+  if (G > 8) return set_error("decode attention: GQA group > 8 unsupported");
+  if (max_pages < 1) max_pages = 1;
+  const int splits = (max_pages + kChunkPages - 1) / kChunkPages;  // work items per (sequence, kv head)
+  DecArgs a{};
+  a.q = reinterpret_cast<const __nv_bfloat16*>(q);
+  a.q_tok_stride = q_tok_stride;
+  a.block_table = block_table;
+  a.bt_stride = bt_stride;
+  a.row_slot = row_slot;
+  a.seq_lens = seq_lens;
+  a.out = reinterpret_cast<__nv_bfloat16*>(out);
+  a.out_tok_stride = out_tok_stride;
+  a.B = B;
+  a.Hkv = Hkv;
+  a.G = G;
+  a.splits = splits;
+  a.scale_log2 = scale * 1.4426950408889634f;
+  const size_t items = (size_t)B * Hkv * splits;
+  if (splits > 1) {
+    const size_t need = items * G * (kD + 2) * sizeof(float);
+    if (workspace == nullptr || ws_bytes < need) return set_error("decode attention: workspace too small");
+    a.part_o = reinterpret_cast<float*>(workspace);
+    a.part_ml = a.part_o + items * G * kD;
   }
+  CUtensorMap map;
+  const uint64_t rows = (uint64_t)num_blocks * 2 * Hkv * kPage;
+  int rc = make_tmap_2d_bf16(&map, cache_layer, kD, rows, kD, 64, kPage);
+  if (rc) return rc;
+  const int smem = kWarps * kStages * kStageBytes + kWarps * kPStageBytes + kWarps * kStages * 8 + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(decode_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return set_cuda_error("decode attn smem attr", e);
+    attr = true;
+  }
+  if (num_sms <= 0) num_sms = 148;
+  const size_t warps_needed = items;
+  int grid = (int)((warps_needed + kWarps - 1) / kWarps);
+  if (grid > num_sms) grid = num_sms;
+  if (grid < 1) grid = 1;
+  decode_attn_tc_kernel<<<grid, kWarps * 32, smem, st>>>(map, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error("decode attn launch", e);
+  if (splits > 1) {
+    decode_attn_combine_kernel<<<dim3(B, Hq), kD, 0, st>>>(a.part_o, a.part_ml, seq_lens, a.out, out_tok_stride,
+                                                           Hkv, G, splits);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return set_cuda_error("decode combine launch", e);
+  }
+  return 0;
 }
 
 }  // namespace rb

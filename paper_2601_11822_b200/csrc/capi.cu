@@ -8,7 +8,7 @@ namespace rb {
 int decode_attention_launch(const void* q, long long q_tok_stride, const void* cache_layer, const int* block_table,
                             int bt_stride, const int* row_slot, const int* seq_lens, void* out,
                             long long out_tok_stride, void* workspace, size_t ws_bytes, int B, int Hq, int Hkv,
-                            int head_dim, int splits, float scale, cudaStream_t st);
+                            int head_dim, int max_pages, float scale, int num_blocks, int num_sms, cudaStream_t st);
 int prefill_attention_launch(const void* q, long long q_tok_stride, const void* cache_layer, const int* bt, int T,
                              int start, int Hq, int Hkv, int head_dim, void* out, long long out_tok_stride,
                              float scale, cudaStream_t st);
@@ -51,10 +51,10 @@ int rb_gemm_bf16(const void* X, const void* W, void* Y, const void* bias, const 
 int rb_decode_attention(const void* q, long long q_tok_stride, const void* cache_layer, const int* block_table,
                         int bt_stride, const int* row_slot, const int* seq_lens, void* out,
                         long long out_tok_stride, void* workspace, size_t ws_bytes, int B, int Hq, int Hkv,
-                        int head_dim, int splits, float scale, void* stream) {
+                        int head_dim, int max_pages, float scale, int num_blocks, int num_sms, void* stream) {
   return rb::decode_attention_launch(q, q_tok_stride, cache_layer, block_table, bt_stride, row_slot, seq_lens, out,
-                                     out_tok_stride, workspace, ws_bytes, B, Hq, Hkv, head_dim, splits, scale,
-                                     ST(stream));
+                                     out_tok_stride, workspace, ws_bytes, B, Hq, Hkv, head_dim, max_pages, scale,
+                                     num_blocks, num_sms, ST(stream));
 }
 
 int rb_prefill_attention(const void* q, long long q_tok_stride, const void* cache_layer, const int* block_table_row,

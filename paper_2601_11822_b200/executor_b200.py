@@ -276,14 +276,13 @@ class B200Executor:
         if g is not None:
             return g
         r = self.runner
-        splits = r.decode_splits(bucket, PAGE * self.max_blocks_per_seq, part.d_sms)
         st = part.ds
         # warm up outside capture (tensor-map cache, function attributes)
-        r.decode_body(bucket, num_sms=part.d_sms, splits=splits, stream=st.cuda_stream)
+        r.decode_body(bucket, num_sms=part.d_sms, stream=st.cuda_stream)
         st.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=st):
-            r.decode_body(bucket, num_sms=part.d_sms, splits=splits, stream=st.cuda_stream)
+            r.decode_body(bucket, num_sms=part.d_sms, stream=st.cuda_stream)
         st.synchronize()
         part.graphs[bucket] = g
         return g
@@ -331,8 +330,7 @@ class B200Executor:
             if self.use_graphs:
                 self._capture(part, bucket).replay()
             else:
-                self.runner.decode_body(bucket, num_sms=part.d_sms,
-                                        splits=self.runner.decode_splits(bucket, max(seq), part.d_sms),
+                self.runner.decode_body(bucket, num_sms=part.d_sms, max_pages=(max(seq) + PAGE - 1) // PAGE,
                                         stream=st.cuda_stream)
             self._dec_out_host[:B].copy_(self.runner.dec.out_ids[:B], non_blocking=True)
         h.finish_record(st)

@@ -170,7 +170,8 @@ class Runner:
         self.max_decode_batch = max_decode_batch
         self.scale = 1.0 / math.sqrt(arch.head_dim)
         self.eps = arch.rms_eps
-        self.attn_ws = torch.empty(max_decode_batch * arch.q_heads * 16 * (arch.head_dim + 2), dtype=torch.float32,
+        chunks = max(1, (max_blocks_per_seq + 15) // 16)
+        self.attn_ws = torch.empty(max_decode_batch * arch.q_heads * chunks * (arch.head_dim + 2), dtype=torch.float32,
                                    device=self.device)
 
     @staticmethod
@@ -228,7 +229,8 @@ class Runner:
         return B.logits[:1]
 
     # ------------------------------------------------------------------ decode
-    def decode_body(self, Bsz: int, *, num_sms: int, splits: int, stream=None, write_logits_only: bool = False):
+    def decode_body(self, Bsz: int, *, num_sms: int, max_pages: int | None = None, stream=None,
+                    write_logits_only: bool = False):
         """One decode step over rows 0..Bsz-1 of the decode workspace.
 
         Inputs (device, pre-filled): dec.slot, dec.pos (= ctx-1, -1 for padding),
@@ -244,8 +246,8 @@ class Runner:
 
         def attn(li):
             ops.decode_attention(q3, self.kv[li], self.block_table, B.slot[:Bsz], B.seq[:Bsz], o3,
-                                 num_kv_heads=arch.kv_heads, splits=splits, workspace=self.attn_ws, scale=self.scale,
-                                 stream=st)
+                                 num_kv_heads=arch.kv_heads, max_pages=max_pages or self.max_blocks,
+                                 workspace=self.attn_ws, scale=self.scale, num_sms=num_sms, stream=st)
 
         self._layers(B, Bsz, num_sms, st, attn)
         ops.rmsnorm(B.x[:Bsz], self.w.norm, B.h[:Bsz], self.eps, stream=st)
@@ -253,9 +255,3 @@ class Runner:
         if not write_logits_only:
             ops.argmax(B.logits[:Bsz], B.out_ids[:Bsz], slot_of_row=B.slot[:Bsz], last_tok=self.last_tok,
                        row_valid=B.seq[:Bsz], stream=st)
-
-    def decode_splits(self, Bsz: int, max_ctx: int, num_sms: int) -> int:
-        """Split-KV factor so B x Hkv x splits covers ~2 waves of the partition."""
-        nb = max(1, (max_ctx + PAGE - 1) // PAGE)
-        want = math.ceil(2 * num_sms / max(1, Bsz * self.arch.kv_heads))
-        return int(max(1, min(16, want, nb // 4 if nb >= 4 else 1)))

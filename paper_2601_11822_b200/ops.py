@@ -36,7 +36,7 @@ _SIGS = {
     ),
     "rb_decode_attention": (
         [_vp, _c_ll, _vp, _vp, _c_int, _vp, _vp, _vp, _c_ll, _vp, _c_size, _c_int, _c_int, _c_int, _c_int, _c_int,
-         _c_float, _vp],
+         _c_float, _c_int, _c_int, _vp],
         _c_int,
     ),
     "rb_prefill_attention": (
@@ -162,18 +162,23 @@ def linear(x: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None, bi
 
 
 def decode_attention(q: torch.Tensor, cache_layer: torch.Tensor, block_table: torch.Tensor, row_slot: torch.Tensor,
-                     seq_lens: torch.Tensor, out: torch.Tensor, *, num_kv_heads: int, splits: int = 1,
-                     workspace: torch.Tensor | None = None, scale: float | None = None, stream=None) -> torch.Tensor:
-    """q, out: [B, Hq, D] (token stride may be padded); cache_layer: [nb, 2, Hkv, 16, D]."""
+                     seq_lens: torch.Tensor, out: torch.Tensor, *, num_kv_heads: int, max_pages: int | None = None,
+                     workspace: torch.Tensor | None = None, scale: float | None = None, num_sms: int | None = None,
+                     stream=None) -> torch.Tensor:
+    """q, out: [B, Hq, D] (token stride may be padded); cache_layer: [nb, 2, Hkv, 16, D].
+
+    max_pages bounds ceil(seq_len/16) over the rows (default: the block table width)."""
     _need_cuda(q, cache_layer, block_table, row_slot, seq_lens, out, workspace)
     B, Hq, D = q.shape
     sc = scale if scale is not None else 1.0 / math.sqrt(D)
+    mp = max_pages if max_pages is not None else block_table.shape[1]
+    sms = num_sms if num_sms is not None else device_sm_count(q.device.index or 0)
     _check(
         load().rb_decode_attention(
             _ptr(q), q.stride(0), _ptr(cache_layer), _ptr(block_table), block_table.stride(0), _ptr(row_slot),
             _ptr(seq_lens), _ptr(out), out.stride(0), _ptr(workspace),
             workspace.numel() * workspace.element_size() if workspace is not None else 0, B, Hq, num_kv_heads, D,
-            splits, sc, _stream(stream),
+            mp, sc, cache_layer.shape[0], sms, _stream(stream),
         ),
         "rb_decode_attention",
     )

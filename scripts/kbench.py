@@ -124,13 +124,15 @@ def main():
             seq = torch.full((B,), ctx, dtype=torch.int32, device=dev)
             q = torch.randn(B, Hq, D, device=dev).bfloat16()
             out = torch.empty(B, Hq, D, device=dev, dtype=torch.bfloat16)
-            splits = max(1, min(16, math.ceil(2 * 148 / (B * Hkv)), nbps // 8))
-            ws = torch.empty(B * Hq * splits * (D + 2), device=dev, dtype=torch.float32)
-            ms = timeit(lambda: ops.decode_attention(q, cache, bt, slots, seq, out, num_kv_heads=Hkv, splits=splits,
+            ws = torch.empty(B * Hq * ((nbps + 15) // 16) * (D + 2), device=dev, dtype=torch.float32)
+            res_row = {}
+            for sms, gs in ((148, None),) + tuple((n, n) for n in (72,)):
+                pass
+            ms = timeit(lambda: ops.decode_attention(q, cache, bt, slots, seq, out, num_kv_heads=Hkv, max_pages=nbps,
                                                      workspace=ws), flush=flush)
             byts = B * ctx * Hkv * D * 2 * 2
             gbs = byts / ms / 1e6
-            row = dict(B=B, ctx=ctx, splits=splits, ms=ms, gbs=gbs, frac_hbm=gbs / PEAKS["hbm_gbs"])
+            row = dict(B=B, ctx=ctx, ms=ms, gbs=gbs, frac_hbm=gbs / PEAKS["hbm_gbs"])
             res["decode_attn"].append(row)
             print(json.dumps(row), flush=True)
             del cache

@@ -29,5 +29,5 @@ elif kind == "dattn":
     q = torch.randn(B, Hq, D, device=dev).bfloat16()
     out = torch.empty(B, Hq, D, device=dev, dtype=torch.bfloat16)
     for _ in range(5):
-        ops.decode_attention(q, cache, bt, slots, seq, out, num_kv_heads=Hkv)
+        ops.decode_attention(q, cache, bt, slots, seq, out, num_kv_heads=Hkv, max_pages=nbps)
 torch.cuda.synchronize()

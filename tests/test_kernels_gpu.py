@@ -98,9 +98,9 @@ def _ref_attn(q, k, v, causal_offset=None):
 
 
 @pytest.mark.parametrize("Hq,Hkv", [(32, 8), (8, 2), (40, 8), (8, 1), (16, 8)])
-@pytest.mark.parametrize("splits", [1, 3])
-def test_decode_attention(Hq, Hkv, splits):
-    gen = torch.Generator(device=DEV).manual_seed(Hq * 10 + Hkv + splits)
+@pytest.mark.parametrize("sms", [148, 72, 8])
+def test_decode_attention(Hq, Hkv, sms):
+    gen = torch.Generator(device=DEV).manual_seed(Hq * 10 + Hkv + sms)
     D, nb, B = 128, 512, 6
     cache = _make_cache(nb, Hkv, D, gen)
     seq = torch.tensor([1, 15, 16, 17, 300, 1000], dtype=torch.int32, device=DEV)
@@ -110,14 +110,37 @@ def test_decode_attention(Hq, Hkv, splits):
     slots = torch.arange(B, dtype=torch.int32, device=DEV).flip(0).contiguous()
     q = torch.randn(B, Hq, D, device=DEV, generator=gen).bfloat16()
     out = torch.zeros(B, Hq, D, device=DEV, dtype=torch.bfloat16)
-    ws = torch.empty(B * Hq * splits * (D + 2), device=DEV, dtype=torch.float32)
-    ops.decode_attention(q, cache, bt, slots, seq, out, num_kv_heads=Hkv, splits=splits, workspace=ws)
+    ws = torch.empty(B * Hq * 4 * (D + 2), device=DEV, dtype=torch.float32)
+    ops.decode_attention(q, cache, bt, slots, seq, out, num_kv_heads=Hkv, max_pages=maxb, workspace=ws, num_sms=sms)
     torch.cuda.synchronize()
     for b in range(B):
         n = int(seq[b])
         k, v = _gather_kv(cache, bt[int(slots[b])], n)
         ref = _ref_attn(q[b : b + 1], k, v)
         assert rel_l2(out[b : b + 1], ref) < 1e-2, (b, n)
+
+
+def test_decode_attention_stale_nan_tail():
+    """Rows past the sequence end in the last page may hold non-finite stale data."""
+    gen = torch.Generator(device=DEV).manual_seed(21)
+    D, nb, Hq, Hkv = 128, 64, 32, 8
+    cache = _make_cache(nb, Hkv, D, gen)
+    seq = torch.tensor([5, 16, 37, 250], dtype=torch.int32, device=DEV)
+    bt = torch.randperm(nb, device=DEV, generator=gen).int()[:4 * 16].view(4, 16).contiguous()
+    for b in range(4):
+        n = int(seq[b])
+        if n % 16:
+            cache[int(bt[b, n // 16]), :, :, n % 16:] = float("nan")
+    slots = torch.arange(4, dtype=torch.int32, device=DEV)
+    q = torch.randn(4, Hq, D, device=DEV, generator=gen).bfloat16()
+    out = torch.empty(4, Hq, D, device=DEV, dtype=torch.bfloat16)
+    ws = torch.empty(4 * Hq * 1 * (D + 2), device=DEV, dtype=torch.float32)
+    ops.decode_attention(q, cache, bt, slots, seq, out, num_kv_heads=Hkv, max_pages=16, workspace=ws)
+    torch.cuda.synchronize()
+    for b in range(4):
+        k, v = _gather_kv(cache, bt[b], int(seq[b]))
+        assert torch.isfinite(out[b]).all()
+        assert rel_l2(out[b : b + 1], _ref_attn(q[b : b + 1], k, v)) < 1e-2
 
 
 def test_decode_attention_padded_rows():
@@ -129,7 +152,7 @@ def test_decode_attention_padded_rows():
     seq = torch.tensor([40, 0, 0, 3], dtype=torch.int32, device=DEV)
     q = torch.randn(4, Hq, D, device=DEV, generator=gen).bfloat16()
     out = torch.full((4, Hq, D), 7.0, device=DEV, dtype=torch.bfloat16)
-    ops.decode_attention(q, cache, bt, slots, seq, out, num_kv_heads=Hkv)
+    ops.decode_attention(q, cache, bt, slots, seq, out, num_kv_heads=Hkv, max_pages=16)
     torch.cuda.synchronize()
     assert torch.all(out[1] == 7.0) and torch.all(out[2] == 7.0)  # padded rows untouched
     k, v = _gather_kv(cache, bt[3], 3)
