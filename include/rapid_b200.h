@@ -33,6 +33,8 @@ const char* rb_last_error(void);
 int rb_device_sm_count(int device, int* out);
 /* Debug: when buf != NULL, every GEMM CTA writes 8 globaltimer stamps to buf[8*cta..]. */
 int rb_debug_gemm_trace(unsigned long long* buf);
+/* Debug: GEMM CTA-pair policy, -1 auto (default), 0 force single-CTA, 1 force 2-CTA pairs. */
+int rb_debug_gemm_pair_mode(int mode);
 
 /* K1/K4 — bf16 linear layer on tcgen05 tensor cores:
  *   Y[t,o] = sum_k X[t,k] W[o,k] (+bias[o]) (+R[t,o])

@@ -25,6 +25,7 @@ int argmax_launch(const void* logits, long long ld, int T, int V, int* out, cons
 int bt_update_launch(const int* upd, int* block_table, int bt_stride, int max_updates, cudaStream_t st);
 int set_last_tok_launch(int* last_tok, int slot, const int* value_ptr, int value, cudaStream_t st);
 int gemm_set_trace(unsigned long long* buf);
+int gemm_set_pair_mode(int mode);
 }  // namespace rb
 
 #define ST(s) reinterpret_cast<cudaStream_t>(s)
@@ -35,6 +36,7 @@ const char* rb_version(void) { return "rapid_b200 0.1 sm_100a"; }
 const char* rb_last_error(void) { return rb::last_error(); }
 
 int rb_debug_gemm_trace(unsigned long long* buf) { return rb::gemm_set_trace(buf); }
+int rb_debug_gemm_pair_mode(int mode) { return rb::gemm_set_pair_mode(mode); }
 
 int rb_device_sm_count(int device, int* out) {
   cudaError_t e = cudaDeviceGetAttribute(out, cudaDevAttrMultiProcessorCount, device);

@@ -5,21 +5,27 @@
 // Realizes the compute term of prefill_time / the weight term of decode_time
 // (reference pkg/src/pdsim/costmodel.py:104 and :130).
 //
-// Two operand mappings onto the UMMA M=128 x N=BN tile:
+// Two operand mappings onto the UMMA tile (M rows x N=BN columns):
 //   normal  (prefill, many tokens): MMA-M = tokens t, MMA-N = features o.
 //   swap-AB (decode, M=B <= 256):   MMA-M = features o, MMA-N = tokens t,
 //            so the tiny batch becomes the UMMA N dimension and the weight
-//            matrix streams through the 128-row A operand (HBM-bound path).
+//            matrix streams through the A operand (HBM-bound path).
 // Both operands are K-major; TMA loads 64-element (128 B) K slabs with the
 // 128B swizzle straight into the UMMA smem layout.
 //
-// Warp roles (192 threads): w0 = TMA producer, w1 = TMEM owner + MMA issuer,
-// w2..w5 = epilogue. Persistent grid, static stride tile schedule, 2 TMEM
-// accumulator buffers so the epilogue of tile i overlaps the MMAs of tile i+1.
-// Epilogue: TMEM -> registers -> per-warp smem tile in OUTPUT orientation ->
-// 16-byte coalesced global stores (8 rows x 64 B per warp instruction), with
-// bias / residual fused in the write-out pass; the same code serves both
-// mappings (swap-AB transposes while staging).
+// kPair = 2 (default): a cluster of two CTAs on an SM pair computes a 256-row
+// tile with tcgen05.mma.cta_group::2 — each CTA stages 128 rows of A and BN/2
+// rows of B (32 KB per 64-wide k-block instead of 48 KB for a 1-CTA 128x256
+// tile), the leader issues the MMAs, both CTAs hold half the accumulator in
+// their TMEM. kPair = 1 keeps the single-CTA M=128 kernel.
+//
+// Warp roles (192 threads/CTA): w0 = TMA producer, w1 = TMEM owner + MMA issuer
+// (leader CTA), w2..w5 = epilogue. Persistent grid, static stride schedule over
+// work units (tile x K-split), 2 TMEM accumulators so the epilogue of unit i
+// overlaps the MMAs of unit i+1. Epilogue: TMEM -> registers -> per-warp smem
+// tile in OUTPUT orientation -> 16-byte coalesced stores with bias / residual
+// fused. Split-K (decode only): fp32 partials in lane-major order, the last
+// arriving split sums all splits in fixed order (deterministic).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
@@ -28,7 +34,7 @@
 
 namespace rb {
 
-constexpr int kBM = 128;
+constexpr int kBM = 128;                // rows of A per CTA
 constexpr int kBK = 64;                 // bf16 elements per 128-byte swizzle row
 constexpr int kABytes = kBM * kBK * 2;  // 16 KB
 constexpr int kThreads = 192;
@@ -37,6 +43,7 @@ constexpr int kStgBytes = 32 * kStgStride * 2;  // per epilogue warp
 
 struct GemmArgs {
   int m_tiles, n_tiles, num_kb, total_tiles;
+  int splits, kb_per_split, total_units;  // unit = tile * splits + split
   int BN, stages;
   int M_valid, N_valid;  // extents in MMA space
   int swap;              // 1: MMA-M = features (output columns), MMA-N = tokens (output rows)
@@ -45,6 +52,8 @@ struct GemmArgs {
   const __nv_bfloat16* residual;
   const __nv_bfloat16* bias;
   uint64_t hint_a, hint_b;
+  float* ws;      // split-K partials [tile][cta][split][BN/32][4 warps][8][32 lanes] float4
+  int* counters;  // per (tile, cta), self-resetting
 };
 
 // Optional timeline trace (debug): per CTA 8 globaltimer stamps.
@@ -134,6 +143,7 @@ __device__ __forceinline__ void epi_block(const GemmArgs& g, __nv_bfloat16* stg,
   __syncwarp();
 }
 
+template <int kPair>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
                              const __grid_constant__ CUtensorMap tmap_b, const GemmArgs g) {
@@ -141,7 +151,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int BN = g.BN;
   const int stages = g.stages;
-  const uint32_t b_bytes = (uint32_t)BN * kBK * 2;
+  const int bn_cta = BN / kPair;                       // B rows staged by this CTA
+  const uint32_t b_bytes = (uint32_t)bn_cta * kBK * 2;
   uint8_t* sA = smem;
   uint8_t* sB = smem + (size_t)stages * kABytes;
   __nv_bfloat16* stg_all = reinterpret_cast<__nv_bfloat16*>(sB + (size_t)stages * b_bytes);
@@ -150,9 +161,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + stages;  // 2
   uint64_t* tempty = tfull + 2;      // 2
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* flag_slot = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = (kPair == 2) ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x / kPair;   // cluster (pair) id
+  const int ncl = gridDim.x / kPair;
   const uint32_t acc_stride = (uint32_t)BN;
   uint32_t tmem_cols = 32;
   while (tmem_cols < 2 * acc_stride) tmem_cols <<= 1;
@@ -167,101 +183,195 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty[a], 4 * kPair);  // one arrive per epilogue warp of every CTA of the pair
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, tmem_cols);
+  if (warp == 1) {
+    if (kPair == 2) tmem_alloc_pair(tmem_slot, tmem_cols);
+    else tmem_alloc(tmem_slot, tmem_cols);
+  }
   tc_fence_before();
   __syncthreads();
+  if (kPair == 2) cluster_sync();  // peers' barriers/TMEM exist before any remote op
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) TRACE(1);
 
   if (warp == 0) {
     if (lane == 0) {
-      // ================= TMA producer =================
+      // ================= TMA producer (both CTAs) =================
+      const uint32_t full_leader0 = (kPair == 2) ? mapa_shared(&full[0], 0) : 0u;
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
+      for (int u = cid; u < g.total_units; u += ncl) {
+        const int t = u / g.splits;
         const int mt = t % g.m_tiles;
         const int nt = t / g.m_tiles;
-        for (int kb = 0; kb < g.num_kb; ++kb) {
+        const int kb0 = (u % g.splits) * g.kb_per_split;
+        const int kb1 = min(g.num_kb, kb0 + g.kb_per_split);
+        const int arow = mt * (kBM * kPair) + (int)rank * kBM;
+        const int brow = nt * BN + (int)rank * bn_cta;
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], kABytes + b_bytes);
-          tma_load_2d(sA + (size_t)stage * kABytes, &tmap_a, &full[stage], kb * kBK, mt * kBM, g.hint_a);
-          tma_load_2d(sB + (size_t)stage * b_bytes, &tmap_b, &full[stage], kb * kBK, nt * BN, g.hint_b);
+          if (kPair == 2) {
+            const uint32_t lbar = full_leader0 + (uint32_t)stage * 8u;
+            if (leader) mbar_arrive_expect_tx(&full[stage], kPair * (kABytes + b_bytes));
+            tma_load_2d_pair(sA + (size_t)stage * kABytes, &tmap_a, lbar, kb * kBK, arow, g.hint_a);
+            tma_load_2d_pair(sB + (size_t)stage * b_bytes, &tmap_b, lbar, kb * kBK, brow, g.hint_b);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], kABytes + b_bytes);
+            tma_load_2d(sA + (size_t)stage * kABytes, &tmap_a, &full[stage], kb * kBK, arow, g.hint_a);
+            tma_load_2d(sB + (size_t)stage * b_bytes, &tmap_b, &full[stage], kb * kBK, brow, g.hint_b);
+          }
           if (++stage == stages) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ================= MMA issuer (single thread) =================
-      const uint32_t idesc = make_idesc_bf16(kBM, BN);
+    if (lane == 0 && leader) {
+      // ================= MMA issuer (single thread of the leader CTA) =================
+      const uint32_t idesc = make_idesc_bf16(kBM * kPair, BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
+      for (int u = cid; u < g.total_units; u += ncl) {
+        const int kb0 = (u % g.splits) * g.kb_per_split;
+        const int kb1 = min(g.num_kb, kb0 + g.kb_per_split);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)acc * acc_stride;
-        for (int kb = 0; kb < g.num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
-          if (t == (int)blockIdx.x && kb == 0) TRACE(2);
-          if (t == (int)blockIdx.x && kb == g.num_kb - 1) TRACE(3);
+          if (u == cid && kb == kb0) TRACE(2);
+          if (u == cid && kb == kb1 - 1) TRACE(3);
           tc_fence_after();
           const uint64_t adesc = make_sdesc_sw128(sA + (size_t)stage * kABytes);
           const uint64_t bdesc = make_sdesc_sw128(sB + (size_t)stage * b_bytes);
 #pragma unroll
           for (int kk = 0; kk < kBK / 16; ++kk) {
             // advance 16 elements (32 bytes) inside the swizzle atom: +2 in 16-byte units
-            umma_bf16(d_tmem, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2), idesc,
-                      (kb > 0 || kk > 0) ? 1u : 0u);
+            const uint32_t accum = (kb > kb0 || kk > 0) ? 1u : 0u;
+            if (kPair == 2)
+              umma_bf16_pair(d_tmem, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2), idesc, accum);
+            else
+              umma_bf16(d_tmem, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2), idesc, accum);
           }
-          umma_commit(&empty[stage]);
+          if (kPair == 2) umma_commit_pair_mc(&empty[stage], 0x3);
+          else umma_commit(&empty[stage]);
           if (++stage == stages) { stage = 0; phase ^= 1; }
         }
-        umma_commit(&tfull[acc]);
+        if (kPair == 2) umma_commit_pair_mc(&tfull[acc], 0x3);
+        else umma_commit(&tfull[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
   } else {
-    // ================= epilogue warps 2..5 =================
+    // ================= epilogue warps 2..5 (both CTAs) =================
     const int q = warp & 3;  // TMEM lane quadrant accessible by this warp
     __nv_bfloat16* stg = stg_all + (size_t)q * (kStgBytes / 2);
+    const uint32_t tempty_leader0 = (kPair == 2) ? mapa_shared(&tempty[0], 0) : 0u;
+    const int nchunk = BN / 32;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
+    for (int u = cid; u < g.total_units; u += ncl) {
+      const int t = u / g.splits;
+      const int sp = u % g.splits;
       const int mt = t % g.m_tiles;
       const int nt = t / g.m_tiles;
-      const int m0 = mt * kBM + q * 32;
+      const int m0 = mt * (kBM * kPair) + (int)rank * kBM + q * 32;
       mbar_wait(&tfull[acc], acc_phase);
-      if (lane == 0 && q == 0 && t == (int)blockIdx.x) TRACE(4);
+      if (lane == 0 && q == 0 && u == cid) TRACE(4);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)acc * acc_stride;
-      if (m0 < g.M_valid) {
-        for (int c = 0; c < BN; c += 32) {
+      auto release_acc = [&]() {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (kPair == 2) mbar_arrive_remote(tempty_leader0 + (uint32_t)acc * 8u);
+          else mbar_arrive(&tempty[acc]);
+        }
+      };
+      if (g.splits == 1) {
+        if (m0 < g.M_valid) {
+          for (int c = 0; c < BN; c += 32) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(tbase + c, v);
+            tmem_ld_wait();
+            if (nt * BN + c < g.N_valid) epi_block(g, stg, lane, m0, nt * BN + c, v);
+          }
+        }
+        release_acc();
+      } else {
+        // ---- deterministic split-K over this CTA's 128-row half of the tile
+        const int region = t * kPair + (int)rank;
+        float* reg_ws = g.ws + (size_t)region * g.splits * kBM * BN;
+        float* mine = reg_ws + (size_t)sp * kBM * BN;
+        for (int c = 0; c < nchunk; ++c) {
           uint32_t v[32];
-          tmem_ld_32x32b_x32(tbase + c, v);
+          tmem_ld_32x32b_x32(tbase + c * 32, v);
           tmem_ld_wait();
-          if (nt * BN + c < g.N_valid) epi_block(g, stg, lane, m0, nt * BN + c, v);
+          // lane-major layout: float4 j of lane l at (j*32 + l) -> 512 contiguous bytes per store
+          float4* dst = reinterpret_cast<float4*>(mine + ((size_t)c * 4 + q) * 1024) + lane;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            dst[j * 32] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                      __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+        }
+        release_acc();
+        __threadfence();
+        named_bar_sync(1, 128);
+        if (q == 0 && lane == 0) {
+          const int prev = atomicAdd(&g.counters[region], 1);
+          const int last = (prev == g.splits - 1);
+          if (last) g.counters[region] = 0;  // re-arm for the next launch / graph replay
+          *flag_slot = last;
+        }
+        named_bar_sync(1, 128);
+        const bool last = *flag_slot != 0;
+        named_bar_sync(1, 128);  // flag consumed before the next unit may overwrite it
+        if (last) {
+          __threadfence();
+          if (m0 < g.M_valid) {
+            for (int c = 0; c < nchunk; ++c) {
+              float acc_v[32];
+#pragma unroll
+              for (int j = 0; j < 32; ++j) acc_v[j] = 0.f;
+              for (int s2 = 0; s2 < g.splits; ++s2) {
+                const float4* src = reinterpret_cast<const float4*>(
+                                        reg_ws + (size_t)s2 * kBM * BN + ((size_t)c * 4 + q) * 1024) + lane;
+                float4 f[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) f[j] = __ldcg(src + j * 32);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  acc_v[4 * j] += f[j].x;
+                  acc_v[4 * j + 1] += f[j].y;
+                  acc_v[4 * j + 2] += f[j].z;
+                  acc_v[4 * j + 3] += f[j].w;
+                }
+              }
+              uint32_t v[32];
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(acc_v[j]);
+              if (nt * BN + c * 32 < g.N_valid) epi_block(g, stg, lane, m0, nt * BN + c * 32, v);
+            }
+          }
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (lane == 0 && q == 0 && t == (int)blockIdx.x) TRACE(5);
+      if (lane == 0 && q == 0 && u == cid) TRACE(5);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
   tc_fence_before();
   __syncthreads();
+  if (kPair == 2) cluster_sync();  // the leader's MMAs into the peer's TMEM are done
   if (threadIdx.x == 0) TRACE(6);
   if (warp == 1) {
     __syncwarp();
-    tmem_dealloc(tmem_base, tmem_cols);
+    if (kPair == 2) tmem_dealloc_pair(tmem_base, tmem_cols);
+    else tmem_dealloc(tmem_base, tmem_cols);
   }
 }
 
@@ -272,14 +382,19 @@ int gemm_set_trace(unsigned long long* buf) {
   return e == cudaSuccess ? 0 : set_cuda_error("gemm trace", e);
 }
 
-static int gemm_smem_bytes(int bn, int stages) {
-  return stages * (kABytes + bn * kBK * 2) + 4 * kStgBytes + 1024 /*align*/ + (2 * stages + 4) * 8 + 16;
+static int gemm_smem_bytes(int b_rows_per_cta, int stages) {
+  return stages * (kABytes + b_rows_per_cta * kBK * 2) + 4 * kStgBytes + 1024 /*align*/ + (2 * stages + 4) * 8 + 32;
+}
+
+static int g_force_pair = -1;  // debug override: -1 auto, 0 single-CTA, 1 CTA pair
+int gemm_set_pair_mode(int mode) {
+  g_force_pair = mode;
+  return 0;
 }
 
 int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, const void* residual, int T,
                      int O, int K, long long ldx, long long ldw, long long ldy, int mode, int num_sms,
                      void* workspace, size_t ws_bytes, int* counters, int counters_len, cudaStream_t stream) {
-  (void)workspace; (void)ws_bytes; (void)counters; (void)counters_len;  // split-K scratch: reserved
   if (T <= 0 || O <= 0) return 0;
   if (K % kBK != 0) return set_error("gemm: K must be a multiple of 64");
   if ((ldx * 2) % 16 || (ldw * 2) % 16) return set_error("gemm: row strides must be 16-byte multiples");
@@ -290,6 +405,7 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
     return set_error("gemm: Y/residual/bias must be 16-byte aligned with ldy % 8 == 0");
   if (mode == 0) mode = (T <= 256) ? 2 : 1;
   const bool swap = (mode == 2);
+  if (num_sms <= 0) num_sms = 148;
   GemmArgs g{};
   const int M = swap ? O : T;  // MMA-space rows
   const int N = swap ? T : O;  // MMA-space cols
@@ -300,16 +416,50 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
   } else {
     BN = 256;
   }
-  const int stage_bytes = kABytes + BN * kBK * 2;
+  // CTA pair whenever the partition has >= 2 SMs and the tile is wide enough to split B
+  // CTA pairs halve the per-SM operand stream of the tensor-bound prefill tiles; decode
+  // (swap-AB) tiles measured faster single (short K-split units, latency-dominated).
+  int pair = (!swap && num_sms >= 2 && M > kBM) ? 2 : 1;
+  if (g_force_pair == 0) pair = 1;
+  if (g_force_pair == 1 && num_sms >= 2 && BN >= 32) pair = 2;
+  const int bn_cta = BN / pair;
+  const int stage_bytes = kABytes + bn_cta * kBK * 2;
   int stages = (200 * 1024 - 4 * kStgBytes) / stage_bytes;
   if (stages > 8) stages = 8;
   if (stages < 2) stages = 2;
   g.BN = BN;
   g.stages = stages;
-  g.m_tiles = (M + kBM - 1) / kBM;
+  g.m_tiles = (M + kBM * pair - 1) / (kBM * pair);
   g.n_tiles = (N + BN - 1) / BN;
   g.num_kb = K / kBK;
   g.total_tiles = g.m_tiles * g.n_tiles;
+  const int slots = num_sms / pair;  // concurrent work-unit slots (clusters)
+  // split-K (decode / swap-AB only) when the tile count under-fills the partition.
+  // Each CTA is bound by its own L2->SMEM stream, so a work unit costs the bytes a CTA
+  // streams ((128 + BN/pair) x K/S x 2) plus, when split, writing its fp32 partial and
+  // the amortised fixed-order re-read (2 x 128 x BN x 4); minimise rounds x unit cost.
+  int splits = 1;
+  if (swap && workspace != nullptr && counters != nullptr && g.total_tiles * pair <= counters_len) {
+    const double stream_bytes = (double)(kBM + bn_cta) * K * 2.0;
+    const double part_bytes = 2.0 * kBM * BN * 4.0;
+    double best = (double)((g.total_tiles + slots - 1) / slots) * stream_bytes;
+    for (int s2 = 2; s2 <= 8; ++s2) {
+      if (g.num_kb / s2 < 4) break;
+      const size_t need = (size_t)g.total_tiles * pair * s2 * kBM * BN * sizeof(float);
+      if (need > ws_bytes) break;
+      const double rounds = (double)((g.total_tiles * s2 + slots - 1) / slots);
+      const double cost = rounds * (stream_bytes / s2 + part_bytes);
+      if (cost < 0.95 * best) {
+        best = cost;
+        splits = s2;
+      }
+    }
+  }
+  g.kb_per_split = (g.num_kb + splits - 1) / splits;
+  g.splits = (g.num_kb + g.kb_per_split - 1) / g.kb_per_split;
+  g.total_units = g.total_tiles * g.splits;
+  g.ws = reinterpret_cast<float*>(workspace);
+  g.counters = counters;
   g.M_valid = M;
   g.N_valid = N;
   g.swap = swap ? 1 : 0;
@@ -324,7 +474,6 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
     g.hint_a = kEvictLast;
     g.hint_b = kEvictNormal;
   }
-  if (num_sms <= 0) num_sms = 148;
 
   CUtensorMap ta, tb;
   const void* a_ptr = swap ? W : X;
@@ -333,20 +482,38 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
   const long long ldb = swap ? ldx : ldw;
   int rc = make_tmap_2d_bf16(&ta, a_ptr, (uint64_t)K, (uint64_t)M, (uint64_t)lda, kBK, kBM);
   if (rc) return rc;
-  rc = make_tmap_2d_bf16(&tb, b_ptr, (uint64_t)K, (uint64_t)N, (uint64_t)ldb, kBK, BN);
+  rc = make_tmap_2d_bf16(&tb, b_ptr, (uint64_t)K, (uint64_t)N, (uint64_t)ldb, kBK, bn_cta);
   if (rc) return rc;
 
-  const int smem = gemm_smem_bytes(BN, stages);
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tcgen05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024);
+  const int smem = gemm_smem_bytes(bn_cta, stages);
+  static bool attr_done[2] = {false, false};
+  if (!attr_done[pair - 1]) {
+    cudaError_t e = cudaFuncSetAttribute(pair == 2 ? gemm_bf16_tcgen05_kernel<2> : gemm_bf16_tcgen05_kernel<1>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return set_cuda_error("gemm: set smem attr", e);
-    attr_done = true;
+    attr_done[pair - 1] = true;
   }
-  int grid = g.total_tiles < num_sms ? g.total_tiles : num_sms;
-  gemm_bf16_tcgen05_kernel<<<grid, kThreads, smem, stream>>>(ta, tb, g);
-  cudaError_t e = cudaGetLastError();
+  int clusters = g.total_units < slots ? g.total_units : slots;
+  if (clusters < 1) clusters = 1;
+  cudaError_t e;
+  if (pair == 2) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * clusters);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, gemm_bf16_tcgen05_kernel<2>, ta, tb, g);
+  } else {
+    gemm_bf16_tcgen05_kernel<1><<<clusters, kThreads, smem, stream>>>(ta, tb, g);
+    e = cudaGetLastError();
+  }
   if (e != cudaSuccess) return set_cuda_error("gemm launch", e);
   return 0;
 }

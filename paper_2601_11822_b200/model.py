@@ -142,6 +142,8 @@ class _Buffers:
         self.slot = torch.zeros(rows, dtype=torch.int32, device=device)
         self.seq = torch.zeros(rows, dtype=torch.int32, device=device)
         self.out_ids = torch.zeros(rows, dtype=torch.int32, device=device)
+        # split-K partials + tile counters of this phase's GEMMs (never shared across streams)
+        self.scratch = ops.GemmScratch(device, ws_bytes=64 << 20, n_counters=8192)
 
 
 class Runner:
@@ -181,19 +183,20 @@ class Runner:
     # ------------------------------------------------------------------ layers
     def _layers(self, B: _Buffers, T: int, num_sms: int, stream, attn_fn):
         arch, W = self.arch, self.w
+        sc = B.scratch
         x, h = B.x[:T], B.h[:T]
         for li, L in enumerate(W.layers):
             ops.rmsnorm(x, L.ln1, h, self.eps, stream=stream)
-            ops.linear(h, L.wqkv, out=B.qkv[:T], bias=L.bqkv, num_sms=num_sms, stream=stream)
+            ops.linear(h, L.wqkv, out=B.qkv[:T], bias=L.bqkv, num_sms=num_sms, scratch=sc, stream=stream)
             ops.rope_cache_write(B.qkv[:T], B.pos[:T], B.slot[:T], self.block_table, self.cos_sin, B.q[:T],
                                  self.kv[li], num_q_heads=arch.q_heads, num_kv_heads=arch.kv_heads,
                                  head_dim=arch.head_dim, stream=stream)
             attn_fn(li)
-            ops.linear(B.attn[:T], L.wo, out=x, residual=x, num_sms=num_sms, stream=stream)
+            ops.linear(B.attn[:T], L.wo, out=x, residual=x, num_sms=num_sms, scratch=sc, stream=stream)
             ops.rmsnorm(x, L.ln2, h, self.eps, stream=stream)
-            ops.linear(h, L.wgu, out=B.gu[:T], num_sms=num_sms, stream=stream)
+            ops.linear(h, L.wgu, out=B.gu[:T], num_sms=num_sms, scratch=sc, stream=stream)
             ops.silu_mul(B.gu[:T], B.act[:T], stream=stream)
-            ops.linear(B.act[:T], L.wd, out=x, residual=x, num_sms=num_sms, stream=stream)
+            ops.linear(B.act[:T], L.wd, out=x, residual=x, num_sms=num_sms, scratch=sc, stream=stream)
 
     # ------------------------------------------------------------------ prefill
     def prefill(self, slot: int, token_ids: torch.Tensor, start: int, *, num_sms: int, stream=None,
@@ -225,7 +228,7 @@ class Runner:
             return None
         last = B.x[T - 1 : T]
         ops.rmsnorm(last, self.w.norm, B.h[:1], self.eps, stream=st)
-        ops.linear(B.h[:1], self.w.lm_head, out=B.logits[:1], num_sms=num_sms, stream=st)
+        ops.linear(B.h[:1], self.w.lm_head, out=B.logits[:1], num_sms=num_sms, scratch=B.scratch, stream=st)
         return B.logits[:1]
 
     # ------------------------------------------------------------------ decode
@@ -251,7 +254,7 @@ class Runner:
 
         self._layers(B, Bsz, num_sms, st, attn)
         ops.rmsnorm(B.x[:Bsz], self.w.norm, B.h[:Bsz], self.eps, stream=st)
-        ops.linear(B.h[:Bsz], self.w.lm_head, out=B.logits[:Bsz], num_sms=num_sms, stream=st)
+        ops.linear(B.h[:Bsz], self.w.lm_head, out=B.logits[:Bsz], num_sms=num_sms, scratch=B.scratch, stream=st)
         if not write_logits_only:
             ops.argmax(B.logits[:Bsz], B.out_ids[:Bsz], slot_of_row=B.slot[:Bsz], last_tok=self.last_tok,
                        row_valid=B.seq[:Bsz], stream=st)
