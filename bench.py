@@ -182,6 +182,8 @@ def main():
     ap.add_argument("--model", default="llama3.1-8b")
     ap.add_argument("--ref-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--arm", action="store_true",
+                    help="cfg 3: adaptive ARM (allocate() per launch) instead of the cfg-2 static split")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -209,17 +211,19 @@ def main():
     duration = args.duration or max(30.0, 8.0 + (args.warmup + args.steps) * 0.02 * 1.6)
     items = synthesize(WorkloadSpec(qps=args.qps, duration_s=duration, seed=42 + rank, mean_prompt_tokens=PROMPT,
                                     mean_output_tokens=OUTPUT, sigma=0.0))
-    ex = B200Executor(arch, seed=rank, static_decode_sms=args.decode_sms, max_batch=256, chunk_tokens=2048,
+    ex = B200Executor(arch, seed=rank, static_decode_sms=None if args.arm else args.decode_sms, max_batch=256,
+                      chunk_tokens=2048,
                       max_context=PROMPT + OUTPUT + 64, num_slots=1024)
     ex.warmup()
-    d_sms = ex._partitions[args.decode_sms].d_sms
-    p_sms = ex._partitions[args.decode_sms].p_sms
+    pkey = None if args.arm else args.decode_sms
+    d_sms = ex._partitions[pkey].d_sms
+    p_sms = ex._partitions[pkey].p_sms
     total = ex.total_sms
-    static = AllocationDecision(AllocationMode.PARTITION, p_sms / total, d_sms / total)
+    static = None if args.arm else AllocationDecision(AllocationMode.PARTITION, p_sms / total, d_sms / total)
     model = arch.model_spec()
     slo = SloSpec(itl_slo_us=SLO_ITL_US)
     engine = RapidEngine(model, b200_spec(), CostParams(), slo, chunk_tokens=2048, max_batch=256, executor=ex,
-                         static_decision=static)
+                         static_decision=None if args.arm else static, record_decisions=args.arm)
 
     # ---- timed window over decode steps, hooked on the executor
     horizon = int(duration * 1e6)
@@ -292,7 +296,7 @@ def main():
     e2e_value = tokens / host_s if complete else 0.0
 
     # live roofline probe of the dominant decode kernel (decode attention)
-    part = ex._partitions[args.decode_sms]
+    part = ex._partitions[pkey]
     mB = int(round(statistics.mean(win["Bs"]))) if win["Bs"] else 64
     mctx = int(round(statistics.mean(win["ctxs"]))) if win["ctxs"] else PROMPT + OUTPUT // 2
     probe = time_decode_attention(ex.runner, part.ds, mB, mctx, part.d_sms)
@@ -326,8 +330,11 @@ def main():
         "dtype": "bf16",
         "data": "synthetic (random-init Llama-3.1-8B weights, synthesize() trace)",
         "config": {
-            "workload": f"cfg2: {args.model} bf16, 1x B200 per replica, static split decode {d_sms} / prefill "
-                        f"{p_sms} SMs, trace in {PROMPT}/out {OUTPUT} sigma=0 at {args.qps} QPS for {duration:.0f} s",
+            "workload": (f"cfg3: {args.model} bf16, adaptive ARM (allocate() at every launch; OVERALLOCATE -> "
+                         f"both phases on {total} SMs, PARTITION -> green-context split)" if args.arm else
+                         f"cfg2: {args.model} bf16, 1x B200 per replica, static split decode {d_sms} / prefill "
+                         f"{p_sms} SMs") + f", trace in {PROMPT}/out {OUTPUT} sigma=0 at {args.qps} QPS for "
+                                         f"{duration:.0f} s",
             "qps_per_replica": args.qps,
             "parallelism": f"replicas x{world}",
             "l2": "inputs > L2 (KV + weights ~30 GB per step); no flush",
@@ -354,6 +361,8 @@ def main():
         "clocks": win.get("clocks", {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}),
         "cpu_baseline": cpu,
         "run_wall_s": t_run,
+        "arm_decisions": ({k: sum(1 for _, d in engine.decision_log if d.mode.value == k)
+                           for k in ("overallocate", "partition")} if args.arm else None),
         "requests": len(engine.requests),
         "finished": sum(1 for r in engine.requests if r.state.value == "finished"),
         "profiles": profile_path,

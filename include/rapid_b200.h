@@ -92,6 +92,61 @@ int rb_argmax(const void* logits, long long ld, int T, int V, int* out, const in
 int rb_block_table_update(const int* upd, int* block_table, int bt_stride, int max_updates, void* stream);
 int rb_set_last_token(int* last_tok, int slot, const int* value_ptr, int value, void* stream);
 
+/* Whole-iteration decoder forward (Llama-3.x / Qwen2 family), launched from
+ * native code: replaces one priced iteration of the reference —
+ * prefill_time (costmodel.py:89-106), decode_time (:109-134) or hybrid_time
+ * (:137-163) — with every kernel of that iteration on `stream`.
+ * Rows [0, n_decode) are single-token decode rows (paged decode attention);
+ * rows [n_decode, rows) are one prefill chunk of slot `prefill_slot` at
+ * positions prefill_start.. (causal over its paged prefix). Host arrays in
+ * rb_model_t hold one device pointer per layer. Graph-capturable. */
+typedef struct {
+  int hidden, layers, q_heads, kv_heads, head_dim, intermediate, vocab;
+  float rms_eps, attn_scale;
+  const void* embed;
+  const void* final_norm;
+  const void* lm_head;
+  const void* const* ln1;   /* [layers] */
+  const void* const* wqkv;  /* [layers] fused q|k|v, [(Hq+2Hkv)*D, H] */
+  const void* const* bqkv;  /* [layers] or NULL (Qwen2 bias) */
+  const void* const* wo;
+  const void* const* ln2;
+  const void* const* wgu;   /* [layers] fused gate|up, [2I, H] */
+  const void* const* wd;
+  void* kv_cache;           /* layer 0 of [L][num_blocks][2][Hkv][16][D] */
+  size_t kv_layer_stride_bytes;
+  int num_blocks;
+  int* block_table;
+  int bt_stride;
+  const float* cos_sin;
+  int* last_tok;
+} rb_model_t;
+
+typedef struct {
+  void *x, *h, *qkv, *q, *attn, *gu, *act, *logits; /* bf16 activations, rows_cap rows */
+  int rows_cap;
+  int *ids, *pos, *slot, *seq, *out_ids;            /* int32 [rows_cap] */
+  void* gemm_ws;
+  size_t gemm_ws_bytes;
+  int* gemm_counters;
+  int gemm_counters_len;
+  void* attn_ws;
+  size_t attn_ws_bytes;
+} rb_workspace_t;
+
+typedef struct {
+  int rows, n_decode, n_prefill;
+  int max_pages;       /* bound on decode rows' ceil(seq/16) */
+  int prefill_slot, prefill_start;
+  int ids_from_slots;  /* decode rows read their input id from last_tok[slot] */
+  int logits_decode;   /* lm_head over the decode rows */
+  int emit_prefill;    /* lm_head over the chunk's last row (appended after the decode rows) */
+  int sample;          /* greedy argmax -> out_ids, scattered into last_tok[slot] */
+  int num_sms;         /* SMs of the partition `stream` runs on */
+} rb_batch_t;
+
+int rb_decoder_forward(const rb_model_t* model, const rb_workspace_t* ws, const rb_batch_t* batch, void* stream);
+
 /* K7 — SM partitioning with CUDA green contexts (replaces the CU-fraction
  * scalars of AllocationDecision, pkg/src/pdsim/core.py:215-245, and the
  * cu_fraction argument of effective_bandwidth/_roofline_us,

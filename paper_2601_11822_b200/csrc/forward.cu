@@ -1,0 +1,115 @@
+// Native decoder-forward driver: one C call launches a whole forward pass.
+//
+// The reference prices a prefill chunk / decode step / fused hybrid iteration
+// as one number (costmodel.py:89-163). Here one rb_decoder_forward() call
+// launches every kernel of that iteration on one stream — the host-side cost
+// of a 32-layer chunk drops from ~300 Python->C calls to one — and the same
+// entry serves all three shapes:
+//   rows [0, n_decode)           one token per sequence, paged decode attention
+//   rows [n_decode, rows)        one chunk of one sequence (causal over its paged prefix)
+// Decode graphs capture this call; hybrid (chunked-prefill) iterations call it
+// with both segments non-empty (K9).
+#include <cuda_runtime.h>
+#include "rb_common.h"
+#include "../../include/rapid_b200.h"
+
+namespace rb {
+int decode_attention_launch(const void* q, long long q_tok_stride, const void* cache_layer, const int* block_table,
+                            int bt_stride, const int* row_slot, const int* seq_lens, void* out,
+                            long long out_tok_stride, void* workspace, size_t ws_bytes, int B, int Hq, int Hkv,
+                            int head_dim, int max_pages, float scale, int num_blocks, int num_sms, cudaStream_t st);
+int prefill_attention_launch(const void* q, long long q_tok_stride, const void* cache_layer, const int* bt, int T,
+                             int start, int Hq, int Hkv, int head_dim, void* out, long long out_tok_stride,
+                             float scale, cudaStream_t st);
+int rmsnorm_launch(const void* x, long long ldx, const void* w, void* y, long long ldy, int T, int H, float eps,
+                   cudaStream_t st);
+int rope_cache_launch(const void* qkv, long long ld_qkv, const int* pos, const int* tok_slot, const int* bt,
+                      int bt_stride, const float* cos_sin, void* q_out, long long ld_q, void* cache_layer, int T,
+                      int Hq, int Hkv, int D, cudaStream_t st);
+int silu_mul_launch(const void* gu, long long ld_gu, void* y, long long ldy, int T, int I, cudaStream_t st);
+int embed_launch(const int* ids, const int* slot_of_row, const int* last_tok, const void* table, void* y, int T, int H,
+                 int* ids_out, cudaStream_t st);
+int argmax_launch(const void* logits, long long ld, int T, int V, int* out, const int* slot_of_row, int* last_tok,
+                  const int* row_valid, cudaStream_t st);
+}  // namespace rb
+
+#define RB_TRY(x)          \
+  do {                     \
+    int _rc = (x);         \
+    if (_rc) return _rc;   \
+  } while (0)
+
+extern "C" int rb_decoder_forward(const rb_model_t* m, const rb_workspace_t* w, const rb_batch_t* b, void* stream) {
+  using namespace rb;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int T = b->rows;
+  if (T <= 0) return 0;
+  if (T > w->rows_cap) return set_error("decoder_forward: rows exceed workspace");
+  const int nd = b->n_decode, np = b->n_prefill;
+  if (nd < 0 || np < 0 || nd + np != T) return set_error("decoder_forward: rows != n_decode + n_prefill");
+  const int H = m->hidden, D = m->head_dim, Hq = m->q_heads, Hkv = m->kv_heads, I = m->intermediate;
+  const int nq = (Hq + 2 * Hkv) * D;
+  const size_t e = 2;  // bf16 bytes
+  char* x = static_cast<char*>(w->x);
+  char* h = static_cast<char*>(w->h);
+  char* qkv = static_cast<char*>(w->qkv);
+  char* q = static_cast<char*>(w->q);
+  char* attn = static_cast<char*>(w->attn);
+  char* gu = static_cast<char*>(w->gu);
+  char* act = static_cast<char*>(w->act);
+  const int sms = b->num_sms;
+  // ---- embedding: decode rows from device slot state, prefill rows from ids[]
+  if (nd > 0) {
+    if (b->ids_from_slots)
+      RB_TRY(embed_launch(nullptr, w->slot, m->last_tok, m->embed, x, nd, H, w->ids, st));
+    else
+      RB_TRY(embed_launch(w->ids, nullptr, nullptr, m->embed, x, nd, H, nullptr, st));
+  }
+  if (np > 0) RB_TRY(embed_launch(w->ids + nd, nullptr, nullptr, m->embed, x + (size_t)nd * H * e, np, H, nullptr, st));
+  for (int l = 0; l < m->layers; ++l) {
+    char* cache = static_cast<char*>(m->kv_cache) + (size_t)l * m->kv_layer_stride_bytes;
+    RB_TRY(rmsnorm_launch(x, H, m->ln1[l], h, H, T, H, m->rms_eps, st));
+    RB_TRY(gemm_bf16_launch(h, m->wqkv[l], qkv, m->bqkv ? m->bqkv[l] : nullptr, nullptr, T, nq, H, H, H, nq, 0, sms,
+                            w->gemm_ws, w->gemm_ws_bytes, w->gemm_counters, w->gemm_counters_len, st));
+    RB_TRY(rope_cache_launch(qkv, nq, w->pos, w->slot, m->block_table, m->bt_stride, m->cos_sin, q, Hq * D, cache, T,
+                             Hq, Hkv, D, st));
+    if (nd > 0)
+      RB_TRY(decode_attention_launch(q, (long long)Hq * D, cache, m->block_table, m->bt_stride, w->slot, w->seq, attn,
+                                     (long long)Hq * D, w->attn_ws, w->attn_ws_bytes, nd, Hq, Hkv, D, b->max_pages,
+                                     m->attn_scale, m->num_blocks, sms, st));
+    if (np > 0)
+      RB_TRY(prefill_attention_launch(q + (size_t)nd * Hq * D * e, (long long)Hq * D, cache,
+                                      m->block_table + (size_t)b->prefill_slot * m->bt_stride, np, b->prefill_start,
+                                      Hq, Hkv, D, attn + (size_t)nd * Hq * D * e, (long long)Hq * D, m->attn_scale,
+                                      st));
+    RB_TRY(gemm_bf16_launch(attn, m->wo[l], x, nullptr, x, T, H, Hq * D, Hq * D, Hq * D, H, 0, sms, w->gemm_ws,
+                            w->gemm_ws_bytes, w->gemm_counters, w->gemm_counters_len, st));
+    RB_TRY(rmsnorm_launch(x, H, m->ln2[l], h, H, T, H, m->rms_eps, st));
+    RB_TRY(gemm_bf16_launch(h, m->wgu[l], gu, nullptr, nullptr, T, 2 * I, H, H, H, 2 * I, 0, sms, w->gemm_ws,
+                            w->gemm_ws_bytes, w->gemm_counters, w->gemm_counters_len, st));
+    RB_TRY(silu_mul_launch(gu, 2 * I, act, I, T, I, st));
+    RB_TRY(gemm_bf16_launch(act, m->wd[l], x, nullptr, x, T, H, I, I, I, H, 0, sms, w->gemm_ws, w->gemm_ws_bytes,
+                            w->gemm_counters, w->gemm_counters_len, st));
+  }
+  // ---- sampling rows: decode rows, plus the chunk's last row when it finishes a prompt
+  int nl = 0;
+  if (b->logits_decode && nd > 0) {
+    RB_TRY(rmsnorm_launch(x, H, m->final_norm, h, H, nd, H, m->rms_eps, st));
+    nl = nd;
+  }
+  if (b->emit_prefill && np > 0) {
+    RB_TRY(rmsnorm_launch(x + (size_t)(T - 1) * H * e, H, m->final_norm, h + (size_t)nl * H * e, H, 1, H, m->rms_eps,
+                          st));
+    nl += 1;
+  }
+  if (nl > 0) {
+    RB_TRY(gemm_bf16_launch(h, m->lm_head, w->logits, nullptr, nullptr, nl, m->vocab, H, H, H, m->vocab, 0, sms,
+                            w->gemm_ws, w->gemm_ws_bytes, w->gemm_counters, w->gemm_counters_len, st));
+    if (b->sample) {
+      // row_valid = seq (padding rows have seq 0); the emitted prefill row uses the slot of row nd
+      RB_TRY(argmax_launch(w->logits, m->vocab, nl, m->vocab, w->out_ids, w->slot, m->last_tok,
+                           b->emit_prefill && np > 0 ? nullptr : w->seq, st));
+    }
+  }
+  return 0;
+}

@@ -18,6 +18,7 @@ HBM layout:
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass
 
@@ -166,7 +167,7 @@ class Runner:
         self.last_tok = torch.zeros(num_slots + 1, dtype=torch.int32, device=self.device)
         mp = max_position or max(PAGE * max_blocks_per_seq + PAGE, 4096)
         self.cos_sin = rope_table(arch, mp).to(self.device)
-        self.pre = _Buffers(arch, max_prefill_tokens, self.device, 1)
+        self.pre = _Buffers(arch, max_prefill_tokens, self.device, max_decode_batch + 1)
         self.dec = _Buffers(arch, max_decode_batch, self.device, max_decode_batch)
         self.max_prefill_tokens = max_prefill_tokens
         self.max_decode_batch = max_decode_batch
@@ -180,23 +181,43 @@ class Runner:
     def kv_bytes_per_block(arch: ArchConfig) -> int:
         return arch.layers * 2 * arch.kv_heads * PAGE * arch.head_dim * 2
 
-    # ------------------------------------------------------------------ layers
-    def _layers(self, B: _Buffers, T: int, num_sms: int, stream, attn_fn):
-        arch, W = self.arch, self.w
-        sc = B.scratch
-        x, h = B.x[:T], B.h[:T]
-        for li, L in enumerate(W.layers):
-            ops.rmsnorm(x, L.ln1, h, self.eps, stream=stream)
-            ops.linear(h, L.wqkv, out=B.qkv[:T], bias=L.bqkv, num_sms=num_sms, scratch=sc, stream=stream)
-            ops.rope_cache_write(B.qkv[:T], B.pos[:T], B.slot[:T], self.block_table, self.cos_sin, B.q[:T],
-                                 self.kv[li], num_q_heads=arch.q_heads, num_kv_heads=arch.kv_heads,
-                                 head_dim=arch.head_dim, stream=stream)
-            attn_fn(li)
-            ops.linear(B.attn[:T], L.wo, out=x, residual=x, num_sms=num_sms, scratch=sc, stream=stream)
-            ops.rmsnorm(x, L.ln2, h, self.eps, stream=stream)
-            ops.linear(h, L.wgu, out=B.gu[:T], num_sms=num_sms, scratch=sc, stream=stream)
-            ops.silu_mul(B.gu[:T], B.act[:T], stream=stream)
-            ops.linear(B.act[:T], L.wd, out=x, residual=x, num_sms=num_sms, scratch=sc, stream=stream)
+    # ------------------------------------------------------------------ native forward plumbing
+    def _model_c(self) -> ops.RbModel:
+        if getattr(self, "_mc", None) is None:
+            a, W = self.arch, self.w
+            L = a.layers
+
+            def arr(get):
+                return (ctypes.c_void_p * L)(*[get(l) for l in W.layers])
+
+            keep = {"ln1": arr(lambda l: l.ln1.data_ptr()), "wqkv": arr(lambda l: l.wqkv.data_ptr()),
+                    "wo": arr(lambda l: l.wo.data_ptr()), "ln2": arr(lambda l: l.ln2.data_ptr()),
+                    "wgu": arr(lambda l: l.wgu.data_ptr()), "wd": arr(lambda l: l.wd.data_ptr())}
+            if a.qkv_bias:
+                keep["bqkv"] = arr(lambda l: l.bqkv.data_ptr())
+            m = ops.RbModel(hidden=a.hidden, layers=L, q_heads=a.q_heads, kv_heads=a.kv_heads, head_dim=a.head_dim,
+                            intermediate=a.intermediate, vocab=a.vocab, rms_eps=a.rms_eps, attn_scale=self.scale,
+                            embed=W.embed.data_ptr(), final_norm=W.norm.data_ptr(), lm_head=W.lm_head.data_ptr(),
+                            kv_cache=self.kv.data_ptr(), kv_layer_stride_bytes=self.kv[0].numel() * 2,
+                            num_blocks=self.num_blocks, block_table=self.block_table.data_ptr(),
+                            bt_stride=self.block_table.stride(0), cos_sin=self.cos_sin.data_ptr(),
+                            last_tok=self.last_tok.data_ptr())
+            for k, v in keep.items():
+                setattr(m, k, ctypes.cast(v, ctypes.POINTER(ctypes.c_void_p)))
+            self._mc = m
+            self._mc_keep = keep
+        return self._mc
+
+    def _ws_c(self, B: "_Buffers") -> ops.RbWorkspace:
+        rows = B.x.shape[0]
+        return ops.RbWorkspace(x=B.x.data_ptr(), h=B.h.data_ptr(), qkv=B.qkv.data_ptr(), q=B.q.data_ptr(),
+                               attn=B.attn.data_ptr(), gu=B.gu.data_ptr(), act=B.act.data_ptr(),
+                               logits=B.logits.data_ptr(), rows_cap=rows, ids=B.ids.data_ptr(), pos=B.pos.data_ptr(),
+                               slot=B.slot.data_ptr(), seq=B.seq.data_ptr(), out_ids=B.out_ids.data_ptr(),
+                               gemm_ws=B.scratch.ws.data_ptr(), gemm_ws_bytes=B.scratch.ws_bytes,
+                               gemm_counters=B.scratch.counters.data_ptr(),
+                               gemm_counters_len=B.scratch.counters.numel(), attn_ws=self.attn_ws.data_ptr(),
+                               attn_ws_bytes=self.attn_ws.numel() * 4)
 
     # ------------------------------------------------------------------ prefill
     def prefill(self, slot: int, token_ids: torch.Tensor, start: int, *, num_sms: int, stream=None,
@@ -209,27 +230,15 @@ class Runner:
             return None
         if T > self.max_prefill_tokens:
             raise ValueError(f"prefill chunk {T} exceeds workspace {self.max_prefill_tokens}")
-        arch, B = self.arch, self.pre
-        st = stream
+        B = self.pre
         B.ids[:T].copy_(token_ids, non_blocking=True)
         torch.arange(start, start + T, dtype=torch.int32, device=self.device, out=B.pos[:T])
         B.slot[:T].fill_(slot)
-        ops.embed(self.w.embed, B.x[:T], ids=B.ids[:T], stream=st)
-        bt_row = self.block_table[slot]
-        q3 = B.q[:T].view(T, arch.q_heads, arch.head_dim)
-        o3 = B.attn[:T].view(T, arch.q_heads, arch.head_dim)
-
-        def attn(li):
-            ops.prefill_attention(q3, self.kv[li], bt_row, start, o3, num_kv_heads=arch.kv_heads, scale=self.scale,
-                                  stream=st)
-
-        self._layers(B, T, num_sms, st, attn)
-        if not logits:
-            return None
-        last = B.x[T - 1 : T]
-        ops.rmsnorm(last, self.w.norm, B.h[:1], self.eps, stream=st)
-        ops.linear(B.h[:1], self.w.lm_head, out=B.logits[:1], num_sms=num_sms, scratch=B.scratch, stream=st)
-        return B.logits[:1]
+        batch = ops.RbBatch(rows=T, n_decode=0, n_prefill=T, max_pages=1, prefill_slot=slot, prefill_start=start,
+                            ids_from_slots=0, logits_decode=0, emit_prefill=1 if logits else 0, sample=0,
+                            num_sms=num_sms)
+        ops.decoder_forward(self._model_c(), self._ws_c(B), batch, stream)
+        return B.logits[:1] if logits else None
 
     # ------------------------------------------------------------------ decode
     def decode_body(self, Bsz: int, *, num_sms: int, max_pages: int | None = None, stream=None,
@@ -240,21 +249,29 @@ class Runner:
         dec.seq (= ctx, 0 for padding). Reads the input token from last_tok[slot],
         writes the greedy token to dec.out_ids and last_tok[slot]. Graph-capturable.
         """
-        arch, B = self.arch, self.dec
-        st = stream
-        ops.embed(self.w.embed, B.x[:Bsz], slot_of_row=B.slot[:Bsz], last_tok=self.last_tok, ids_out=B.ids[:Bsz],
-                  stream=st)
-        q3 = B.q[:Bsz].view(Bsz, arch.q_heads, arch.head_dim)
-        o3 = B.attn[:Bsz].view(Bsz, arch.q_heads, arch.head_dim)
+        batch = ops.RbBatch(rows=Bsz, n_decode=Bsz, n_prefill=0, max_pages=max_pages or self.max_blocks,
+                            prefill_slot=0, prefill_start=0, ids_from_slots=1, logits_decode=1, emit_prefill=0,
+                            sample=0 if write_logits_only else 1, num_sms=num_sms)
+        ops.decoder_forward(self._model_c(), self._ws_c(self.dec), batch, stream)
 
-        def attn(li):
-            ops.decode_attention(q3, self.kv[li], self.block_table, B.slot[:Bsz], B.seq[:Bsz], o3,
-                                 num_kv_heads=arch.kv_heads, max_pages=max_pages or self.max_blocks,
-                                 workspace=self.attn_ws, scale=self.scale, num_sms=num_sms, stream=st)
-
-        self._layers(B, Bsz, num_sms, st, attn)
-        ops.rmsnorm(B.x[:Bsz], self.w.norm, B.h[:Bsz], self.eps, stream=st)
-        ops.linear(B.h[:Bsz], self.w.lm_head, out=B.logits[:Bsz], num_sms=num_sms, scratch=B.scratch, stream=st)
-        if not write_logits_only:
-            ops.argmax(B.logits[:Bsz], B.out_ids[:Bsz], slot_of_row=B.slot[:Bsz], last_tok=self.last_tok,
-                       row_valid=B.seq[:Bsz], stream=st)
+    # ------------------------------------------------------------------ hybrid (K9)
+    def hybrid(self, n_decode: int, slot: int, start: int, chunk_ids: torch.Tensor | None, *, emit: bool,
+               num_sms: int, max_pages: int, stream=None) -> None:
+        """One fused chunked-prefill iteration in the `pre` workspace: rows [0, n_decode)
+        are decode rows (slot/pos/seq pre-filled by the caller), rows after them the
+        chunk of `slot` at positions start..; when `emit`, the chunk's last row is
+        sampled too (appended after the decode rows in out_ids)."""
+        B = self.pre
+        T = 0 if chunk_ids is None else int(chunk_ids.shape[0])
+        rows = n_decode + T
+        if rows > self.max_prefill_tokens:
+            raise ValueError("hybrid iteration exceeds the workspace")
+        if T:
+            B.ids[n_decode:rows].copy_(chunk_ids, non_blocking=True)
+            torch.arange(start, start + T, dtype=torch.int32, device=self.device, out=B.pos[n_decode:rows])
+            B.slot[n_decode:rows].fill_(slot)
+            B.seq[n_decode:rows].fill_(1)
+        batch = ops.RbBatch(rows=rows, n_decode=n_decode, n_prefill=T, max_pages=max_pages, prefill_slot=slot,
+                            prefill_start=start, ids_from_slots=1, logits_decode=1, emit_prefill=1 if emit else 0,
+                            sample=1, num_sms=num_sms)
+        ops.decoder_forward(self._model_c(), self._ws_c(B), batch, stream)

@@ -62,7 +62,40 @@ _SIGS = {
     "rb_green_destroy": ([_vp], _c_int),
 }
 
+class RbModel(ctypes.Structure):
+    """Mirror of rb_model_t (include/rapid_b200.h)."""
+
+    _fields_ = [(n, _c_int) for n in ("hidden", "layers", "q_heads", "kv_heads", "head_dim", "intermediate",
+                                      "vocab")] + [
+        ("rms_eps", _c_float), ("attn_scale", _c_float), ("embed", _vp), ("final_norm", _vp), ("lm_head", _vp),
+        ("ln1", ctypes.POINTER(_vp)), ("wqkv", ctypes.POINTER(_vp)), ("bqkv", ctypes.POINTER(_vp)),
+        ("wo", ctypes.POINTER(_vp)), ("ln2", ctypes.POINTER(_vp)), ("wgu", ctypes.POINTER(_vp)),
+        ("wd", ctypes.POINTER(_vp)), ("kv_cache", _vp), ("kv_layer_stride_bytes", _c_size), ("num_blocks", _c_int),
+        ("block_table", _vp), ("bt_stride", _c_int), ("cos_sin", _vp), ("last_tok", _vp)]
+
+
+class RbWorkspace(ctypes.Structure):
+    _fields_ = [(n, _vp) for n in ("x", "h", "qkv", "q", "attn", "gu", "act", "logits")] + [("rows_cap", _c_int)] + [
+        (n, _vp) for n in ("ids", "pos", "slot", "seq", "out_ids")] + [
+        ("gemm_ws", _vp), ("gemm_ws_bytes", _c_size), ("gemm_counters", _vp), ("gemm_counters_len", _c_int),
+        ("attn_ws", _vp), ("attn_ws_bytes", _c_size)]
+
+
+class RbBatch(ctypes.Structure):
+    _fields_ = [(n, _c_int) for n in ("rows", "n_decode", "n_prefill", "max_pages", "prefill_slot", "prefill_start",
+                                      "ids_from_slots", "logits_decode", "emit_prefill", "sample", "num_sms")]
+
+
+_SIGS["rb_decoder_forward"] = ([ctypes.POINTER(RbModel), ctypes.POINTER(RbWorkspace), ctypes.POINTER(RbBatch), _vp],
+                               _c_int)
+
 EXPORTED_SYMBOLS = tuple(_SIGS)
+
+
+def decoder_forward(model: RbModel, ws: RbWorkspace, batch: RbBatch, stream=None) -> None:
+    """One whole forward iteration launched natively (rb_decoder_forward)."""
+    _check(load().rb_decoder_forward(ctypes.byref(model), ctypes.byref(ws), ctypes.byref(batch), _stream(stream)),
+           "rb_decoder_forward")
 
 
 def load(path: str | Path | None = None) -> ctypes.CDLL:
