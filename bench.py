@@ -182,6 +182,7 @@ def main():
     ap.add_argument("--model", default="llama3.1-8b")
     ap.add_argument("--ref-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--engine", default="rapid", help="rapid | hybrid-<chunk> (same-engine chunked-prefill comparator)")
     ap.add_argument("--arm", action="store_true",
                     help="cfg 3: adaptive ARM (allocate() per launch) instead of the cfg-2 static split")
     args = ap.parse_args()
@@ -198,7 +199,8 @@ def main():
     from paper_2601_11822_b200.arm import CostParams
     from paper_2601_11822_b200.clock import RealTimeLoop
     from paper_2601_11822_b200.engines.rapid import RapidEngine
-    from paper_2601_11822_b200.executor_b200 import B200Executor
+    from paper_2601_11822_b200.engines.hybrid import HybridEngine
+    from paper_2601_11822_b200.executor_b200 import B200Executor, HybridB200Executor
     from paper_2601_11822_b200.harness import check_invariants
     from paper_2601_11822_b200.slo import SloSpec, percentile_nearest_rank, summarize
     from paper_2601_11822_b200.specs import ARCHS, AllocationDecision, AllocationMode, b200_spec
@@ -211,9 +213,15 @@ def main():
     duration = args.duration or max(30.0, 8.0 + (args.warmup + args.steps) * 0.02 * 1.6)
     items = synthesize(WorkloadSpec(qps=args.qps, duration_s=duration, seed=42 + rank, mean_prompt_tokens=PROMPT,
                                     mean_output_tokens=OUTPUT, sigma=0.0))
-    ex = B200Executor(arch, seed=rank, static_decode_sms=None if args.arm else args.decode_sms, max_batch=256,
-                      chunk_tokens=2048,
-                      max_context=PROMPT + OUTPUT + 64, num_slots=1024)
+    hybrid = args.engine.startswith("hybrid-")
+    if hybrid:
+        args.arm = True  # one fused stream on the whole device; no split
+        hchunk = int(args.engine.split("-", 1)[1])
+        ex = HybridB200Executor(arch, seed=rank, max_batch=256, chunk_tokens=hchunk, max_context=PROMPT + OUTPUT + 64,
+                                num_slots=1024)
+    else:
+        ex = B200Executor(arch, seed=rank, static_decode_sms=None if args.arm else args.decode_sms, max_batch=256,
+                          chunk_tokens=2048, max_context=PROMPT + OUTPUT + 64, num_slots=1024)
     ex.warmup()
     pkey = None if args.arm else args.decode_sms
     d_sms = ex._partitions[pkey].d_sms
@@ -222,20 +230,24 @@ def main():
     static = None if args.arm else AllocationDecision(AllocationMode.PARTITION, p_sms / total, d_sms / total)
     model = arch.model_spec()
     slo = SloSpec(itl_slo_us=SLO_ITL_US)
-    engine = RapidEngine(model, b200_spec(), CostParams(), slo, chunk_tokens=2048, max_batch=256, executor=ex,
-                         static_decision=None if args.arm else static, record_decisions=args.arm)
+    if hybrid:
+        engine = HybridEngine(model, b200_spec(), CostParams(), slo, chunk_tokens=hchunk, max_batch=256, executor=ex)
+    else:
+        engine = RapidEngine(model, b200_spec(), CostParams(), slo, chunk_tokens=2048, max_batch=256, executor=ex,
+                             static_decision=None if args.arm else static, record_decisions=args.arm)
 
     # ---- timed window over decode steps, hooked on the executor
     horizon = int(duration * 1e6)
     win = {"start_handle": None, "end_handle": None, "tokens": 0, "steps": 0, "host0": None, "host1": None,
            "h2d0": 0, "h2d1": 0, "d2h0": 0, "d2h1": 0, "launch0": 0, "launch1": 0, "Bs": [], "ctxs": []}
     clocks = ClockSampler(local)
-    orig_launch = ex.launch_decode
-    orig_finish = ex.finish_decode
+    launch_name, finish_name = ("launch_hybrid", "finish_hybrid") if hybrid else ("launch_decode", "finish_decode")
+    orig_launch = getattr(ex, launch_name)
+    orig_finish = getattr(ex, finish_name)
     loop_ref = {}
 
-    def launch_decode(members, decision, co):
-        h = orig_launch(members, decision, co)
+    def launch_decode(members, *a):
+        h = orig_launch(members, *a)
         st = win
         steady = loop_ref["loop"].clock_us() >= 0.25 * horizon
         if st["start_handle"] is None and ex.decode_steps > args.warmup and steady:
@@ -256,13 +268,15 @@ def main():
         orig_finish(h)
         if getattr(h, "_win", False):
             win["tokens"] += sum(1 for lame in h.lame if not lame)
+            if h.kind == "hybrid" and getattr(h, "req", None) is not None:
+                win["tokens"] += 1  # first token of the request whose prompt this chunk finished
             if h is win["end_handle"]:
                 win["host1"] = time.perf_counter()
                 win["h2d1"], win["d2h1"], win["launch1"] = ex.h2d_bytes, ex.d2h_bytes, ex.gpu_launches
                 win["clocks"] = clocks.stop()
 
-    ex.launch_decode = launch_decode
-    ex.finish_decode = finish_decode
+    setattr(ex, launch_name, launch_decode)
+    setattr(ex, finish_name, finish_decode)
 
     if world > 1:
         torch.distributed.barrier()
@@ -338,7 +352,9 @@ def main():
             "qps_per_replica": args.qps,
             "parallelism": f"replicas x{world}",
             "l2": "inputs > L2 (KV + weights ~30 GB per step); no flush",
-            "step": "one decode iteration (CUDA-graph replay); prefill runs concurrently on its partition",
+            "step": ("one fused hybrid iteration (decode rows + one prefill chunk)" if hybrid else
+                     "one decode iteration (CUDA-graph replay); prefill runs concurrently on its partition"),
+            "engine": args.engine,
         },
         "p50_ttft_ms": summ.ttft_p50_us / 1e3,
         "p99_itl_ms": summ.itl_p99_us / 1e3,
@@ -362,7 +378,7 @@ def main():
         "cpu_baseline": cpu,
         "run_wall_s": t_run,
         "arm_decisions": ({k: sum(1 for _, d in engine.decision_log if d.mode.value == k)
-                           for k in ("overallocate", "partition")} if args.arm else None),
+                           for k in ("overallocate", "partition")} if getattr(engine, "decision_log", None) else None),
         "requests": len(engine.requests),
         "finished": sum(1 for r in engine.requests if r.state.value == "finished"),
         "profiles": profile_path,

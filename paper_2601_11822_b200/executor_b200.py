@@ -353,7 +353,7 @@ class B200Executor:
 
     # ------------------------------------------------------------------ hybrid (K9 fused iteration)
     def launch_hybrid(self, members, head, written, chunk, target):
-        raise NotImplementedError("hybrid GPU iteration: see executor_b200.HybridB200Executor")
+        raise NotImplementedError("fused hybrid iterations run on HybridB200Executor")
 
     def finish_hybrid(self, handle) -> None:
         pass
@@ -371,3 +371,93 @@ class B200Executor:
         torch.cuda.synchronize()
         for p in self._partitions.values():
             p.graphs.clear()
+
+
+class HybridB200Executor(B200Executor):
+    """Same-engine hybrid batching (chunked prefill) on the B200 — the comparator.
+
+    One fused iteration per launch on the whole device (K9): decode rows of all
+    running sequences plus one prefill chunk share every GEMM; attention splits
+    into the paged decode kernel (rows 0..B-1) and the chunk's causal kernel.
+    Token-position contract of hybrid mode: the prefill
+    computes every context position and its last chunk samples y1 from the
+    final position (reference hybrid.py:144-155); a decode row at context c
+    consumes the token at position c-1 and writes its KV there.
+    """
+
+    def __init__(self, arch: ArchConfig, weights: DecoderWeights | None = None, **kw):
+        kw.pop("static_decode_sms", None)
+        kw.setdefault("chunk_tokens", 512)
+        super().__init__(arch, weights, static_decode_sms=None, **kw)
+        cap = self.runner.max_prefill_tokens
+        self._hyb_host = torch.zeros(3 * cap, dtype=torch.int32, pin_memory=True)
+        self._hyb_dev = torch.zeros(3 * cap, dtype=torch.int32, device=self.device)
+        pre = self.runner.pre
+        pre.slot = self._hyb_dev[0:cap]
+        pre.pos = self._hyb_dev[cap:2 * cap]
+        pre.seq = self._hyb_dev[2 * cap:3 * cap]
+        self._hyb_out_host = torch.zeros(cap, dtype=torch.int32, pin_memory=True)
+
+    def warmup(self, decode_sms_list=None) -> None:
+        pass  # fused iterations are not graph-captured (shape changes every iteration)
+
+    def _flush_all(self, stream) -> None:
+        self._upd["decode"].extend(self._upd["prefill"])
+        self._upd["prefill"].clear()
+        self._flush_updates("decode", stream)
+
+    def launch_hybrid(self, members, head, written: int, chunk: int, target: int) -> GpuHandle:
+        part = self._partitions[None]
+        st = part.ds
+        h = GpuHandle("hybrid", st, 1.0)
+        self._flush_all(st)
+        B = len(members)
+        cap = self.runner.max_prefill_tokens
+        hb = self._hyb_host
+        slots = [self._slot_of[r.id] for r in members]
+        ctxs = [r.context_tokens for r in members]
+        if B:
+            hb[0:B].copy_(torch.tensor(slots, dtype=torch.int32))
+            hb[cap:cap + B].copy_(torch.tensor([c - 1 for c in ctxs], dtype=torch.int32))
+            hb[2 * cap:2 * cap + B].copy_(torch.tensor(ctxs, dtype=torch.int32))
+        emit = False
+        chunk_dev = None
+        hslot = 0
+        if head is not None and chunk > 0:
+            hslot = self._slot_of[head.id]
+            ids = self._context_ids(head, written, written + chunk)
+            self._pre_ids_host[:chunk].copy_(ids)
+            emit = written + chunk == target
+        with torch.cuda.stream(st):
+            if B:
+                for k in range(3):
+                    self._hyb_dev[k * cap:k * cap + B].copy_(hb[k * cap:k * cap + B], non_blocking=True)
+            if head is not None and chunk > 0:
+                self._pre_ids_dev[:chunk].copy_(self._pre_ids_host[:chunk], non_blocking=True)
+                chunk_dev = self._pre_ids_dev[:chunk]
+            max_pages = max([(c + PAGE - 1) // PAGE for c in ctxs], default=1)
+            self.runner.hybrid(B, hslot, written, chunk_dev, emit=emit, num_sms=part.d_sms, max_pages=max_pages,
+                               stream=st.cuda_stream)
+            n_out = B + (1 if emit else 0)
+            if n_out:
+                self._hyb_out_host[:n_out].copy_(self.runner.pre.out_ids[:n_out], non_blocking=True)
+        h.finish_record(st)
+        h.members = tuple(members)
+        h.lame = [False] * B
+        h.req = head if emit else None
+        self.h2d_bytes += 12 * B + 4 * chunk
+        self.d2h_bytes += 4 * (B + (1 if emit else 0))
+        self.decode_steps += 1
+        self.gpu_launches += 2 + 9 * self.arch.layers + 4
+        return h
+
+    def finish_hybrid(self, handle) -> None:
+        if handle is None:
+            return
+        B = len(handle.members)
+        out = self._hyb_out_host[: B + (1 if handle.req is not None else 0)].tolist()
+        for r, tok in zip(handle.members, out):
+            self.generated.setdefault(r.id, []).append(tok)
+        if handle.req is not None:
+            self.generated.setdefault(handle.req.id, []).append(out[B])
+        self.step_log.append((B, handle.gpu_us, handle.launch_ns))

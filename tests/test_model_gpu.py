@@ -161,3 +161,39 @@ def test_rapid_realtime_end_to_end_matches_oracle(tiny):
     # flips only happen inside the bf16 rounding band; ~4% of steps have a gap that small
     assert flips <= 0.1 * (exact + flips), (exact, flips)
     ex.close()
+
+
+def test_hybrid_realtime_end_to_end_matches_oracle(tiny):
+    """Same-engine hybrid batching (fused decode rows + prefill chunk per
+    iteration) on the B200: invariants hold, first tokens come from the chunk
+    that finishes each prompt, and all tokens pass the teacher-forced check."""
+    from paper_2601_11822_b200.arm import CostParams
+    from paper_2601_11822_b200.engines.hybrid import HybridEngine
+    from paper_2601_11822_b200.executor_b200 import HybridB200Executor
+    from paper_2601_11822_b200.harness import run_items
+    from paper_2601_11822_b200.slo import SloSpec
+    from paper_2601_11822_b200.specs import b200_spec
+    from paper_2601_11822_b200.traffic import WorkloadSpec, prompt_token_ids, synthesize
+
+    arch, st, orc, w = tiny
+    items = synthesize(WorkloadSpec(qps=16.0, duration_s=4.0, seed=0, mean_prompt_tokens=64,
+                                    mean_output_tokens=16))[:24]
+    ex = HybridB200Executor(arch, weights=w, max_batch=32, chunk_tokens=64, num_blocks=600, max_context=1024,
+                            num_slots=64)
+    model = arch.model_spec()
+    slo = SloSpec(itl_slo_us=50_000)
+    res = run_items("hybrid-64", items, model, b200_spec(), CostParams(), slo,
+                    engine_factory=lambda: HybridEngine(model, b200_spec(), CostParams(), slo, chunk_tokens=64,
+                                                        max_batch=32, executor=ex))
+    done = [r for r in res.engine.requests if r.state.value == "finished"]
+    assert len(done) == len(items)
+    exact = flips = 0
+    for r in done:
+        prompt = prompt_token_ids(r.id, r.prompt_tokens, arch.vocab)
+        assert len(ex.generated[r.id]) == r.output_tokens
+        e, f = teacher_forced_check(orc, prompt, ex.generated[r.id])
+        exact += e
+        flips += f
+    print(f"hybrid teacher-forced: {exact} exact, {flips} near-tie flips")
+    assert flips <= 0.1 * (exact + flips), (exact, flips)
+    ex.close()
