@@ -9,7 +9,8 @@
 // cp.async.bulk.tensor box {64, 16} with the 128B swizzle, so every ldmatrix
 // below is bank-conflict free.
 //
-// Work decomposition: item = (sequence b, kv head h, chunk c of 16 pages).
+// Work decomposition: item = (sequence b, kv head h, chunk c of `chunk_pages`
+// pages); the host picks whole sequences when B x Hkv fills the partition.
 // Persistent grid; every warp owns a private STAGES-deep smem ring and streams
 // the pages of its items (item = global_warp, +num_warps, ...) back to back:
 // lane 0 keeps STAGES pages in flight across item boundaries.
@@ -32,7 +33,6 @@ namespace rb {
 
 constexpr int kD = 128;
 constexpr int kPage = 16;
-constexpr int kChunkPages = 16;           // pages per work item (256 tokens)
 constexpr int kWarps = 8;
 constexpr int kStages = 3;
 constexpr int kStageBytes = 4 * 2048;     // K lo/hi + V lo/hi, 16 rows x 128 B each
@@ -74,7 +74,7 @@ struct DecArgs {
   long long out_tok_stride;
   float* part_o;   // [items][G][128]
   float* part_ml;  // [items][G][2]
-  int B, Hkv, G, splits;
+  int B, Hkv, G, splits, chunk_pages;
   float scale_log2;
 };
 
@@ -87,8 +87,8 @@ __device__ __forceinline__ void item_pages(const DecArgs& a, int item, int& b, i
   b = bh / a.Hkv;
   n = a.seq_lens[b];
   const int nb = (n + kPage - 1) / kPage;
-  p0 = c * kChunkPages;
-  p1 = min(nb, p0 + kChunkPages);
+  p0 = c * a.chunk_pages;
+  p1 = min(nb, p0 + a.chunk_pages);
 }
 
 __global__ void __launch_bounds__(kWarps * 32, 1)
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       l0 += __shfl_xor_sync(0xffffffffu, l0, off);
       l1 += __shfl_xor_sync(0xffffffffu, l1, off);
     }
-    const int nchunks = ((n + kPage - 1) / kPage + kChunkPages - 1) / kChunkPages;
+    const int nchunks = ((n + kPage - 1) / kPage + a.chunk_pages - 1) / a.chunk_pages;
     const int hd0 = 2 * t, hd1 = 2 * t + 1;
     if (nchunks == 1) {
       const float i0 = l0 > 0.f ? 1.f / l0 : 0.f, i1 = l1 > 0.f ? 1.f / l1 : 0.f;
@@ -294,12 +294,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 // merges the chunk partials of multi-chunk sequences; grid (B, Hq), 128 threads
 __global__ void decode_attn_combine_kernel(const float* __restrict__ part_o, const float* __restrict__ part_ml,
                                            const int* __restrict__ seq_lens, __nv_bfloat16* __restrict__ out,
-                                           long long out_tok_stride, int Hkv, int G, int splits) {
+                                           long long out_tok_stride, int Hkv, int G, int splits,
+                                           int chunk_pages) {
   const int b = blockIdx.x;
   const int hq = blockIdx.y;
   const int d = threadIdx.x;
   const int n = seq_lens[b];
-  const int nchunks = ((n + kPage - 1) / kPage + kChunkPages - 1) / kChunkPages;
+  const int nchunks = ((n + kPage - 1) / kPage + chunk_pages - 1) / chunk_pages;
   if (n <= 0 || nchunks <= 1) return;
   const int h = hq / G, hd = hq % G;
   float mx = -FLT_MAX;
@@ -329,7 +330,19 @@ int decode_attention_launch(const void* q, long long q_tok_stride, const void* c
   const int G = Hq / Hkv;
   if (G > 8) return set_error("decode attention: GQA group > 8 unsupported");
   if (max_pages < 1) max_pages = 1;
-  const int splits = (max_pages + kChunkPages - 1) / kChunkPages;  // work items per (sequence, kv head)
+  if (num_sms <= 0) num_sms = 148;
+  // Work-item size: whole sequences when (B x Hkv) already gives every warp of the
+  // partition ~2 items (no partials, no combine pass); otherwise cut sequences into
+  // chunks so there are ~4 items per warp (load balance for long contexts / small B).
+  const long long warps = (long long)num_sms * kWarps;
+  const long long seqs = (long long)B * Hkv;
+  int chunk_pages = max_pages;
+  if (seqs < 2 * warps) {
+    chunk_pages = (int)((max_pages * seqs + 4 * warps - 1) / (4 * warps));
+    if (chunk_pages < 8) chunk_pages = 8;
+    if (chunk_pages > max_pages) chunk_pages = max_pages;
+  }
+  const int splits = (max_pages + chunk_pages - 1) / chunk_pages;  // work items per (sequence, kv head)
   DecArgs a{};
   a.q = reinterpret_cast<const __nv_bfloat16*>(q);
   a.q_tok_stride = q_tok_stride;
@@ -343,6 +356,7 @@ int decode_attention_launch(const void* q, long long q_tok_stride, const void* c
   a.Hkv = Hkv;
   a.G = G;
   a.splits = splits;
+  a.chunk_pages = chunk_pages;
   a.scale_log2 = scale * 1.4426950408889634f;
   const size_t items = (size_t)B * Hkv * splits;
   if (splits > 1) {
@@ -362,7 +376,6 @@ int decode_attention_launch(const void* q, long long q_tok_stride, const void* c
     if (e != cudaSuccess) return set_cuda_error("decode attn smem attr", e);
     attr = true;
   }
-  if (num_sms <= 0) num_sms = 148;
   const size_t warps_needed = items;
   int grid = (int)((warps_needed + kWarps - 1) / kWarps);
   if (grid > num_sms) grid = num_sms;
@@ -372,7 +385,7 @@ int decode_attention_launch(const void* q, long long q_tok_stride, const void* c
   if (e != cudaSuccess) return set_cuda_error("decode attn launch", e);
   if (splits > 1) {
     decode_attn_combine_kernel<<<dim3(B, Hq), kD, 0, st>>>(a.part_o, a.part_ml, seq_lens, a.out, out_tok_stride,
-                                                           Hkv, G, splits);
+                                                           Hkv, G, splits, chunk_pages);
     e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error("decode combine launch", e);
   }

@@ -173,8 +173,9 @@ class Runner:
         self.max_decode_batch = max_decode_batch
         self.scale = 1.0 / math.sqrt(arch.head_dim)
         self.eps = arch.rms_eps
-        chunks = max(1, (max_blocks_per_seq + 15) // 16)
-        self.attn_ws = torch.empty(max_decode_batch * arch.q_heads * chunks * (arch.head_dim + 2), dtype=torch.float32,
+        chunks = max(1, (max_blocks_per_seq + 7) // 8)  # decode attention splits <= ceil(pages / 8)
+        self.attn_ws = torch.zeros(max_decode_batch * arch.q_heads * chunks * (arch.head_dim + 2),
+                                   dtype=torch.float32,
                                    device=self.device)
 
     @staticmethod

@@ -124,7 +124,7 @@ def main():
             seq = torch.full((B,), ctx, dtype=torch.int32, device=dev)
             q = torch.randn(B, Hq, D, device=dev).bfloat16()
             out = torch.empty(B, Hq, D, device=dev, dtype=torch.bfloat16)
-            ws = torch.empty(B * Hq * ((nbps + 15) // 16) * (D + 2), device=dev, dtype=torch.float32)
+            ws = torch.zeros(B * Hq * ((nbps + 7) // 8) * (D + 2), device=dev, dtype=torch.float32)
             res_row = {}
             for sms, gs in ((148, None),) + tuple((n, n) for n in (72,)):
                 pass

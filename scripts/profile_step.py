@@ -41,6 +41,7 @@ ids = torch.randint(0, arch.vocab, (args.T,), dtype=torch.int32, device="cuda")
 torch.cuda.synchronize()
 ev = {}
 for i in range(args.reps):
+    torch.cuda.nvtx.range_push(f"rep{i}")
     if args.what in ("both", "decode"):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(ds)
@@ -54,6 +55,8 @@ for i in range(args.reps):
             r.prefill(args.B, ids, 0, num_sms=gs.sms[1], stream=ps.cuda_stream)
         e1.record(ps)
         ev.setdefault("prefill", []).append((e0, e1))
+    torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
 torch.cuda.synchronize()
 for k, v in ev.items():
     print(k, [round(a.elapsed_time(b), 3) for a, b in v], "ms")

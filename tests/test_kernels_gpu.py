@@ -110,7 +110,7 @@ def test_decode_attention(Hq, Hkv, sms):
     slots = torch.arange(B, dtype=torch.int32, device=DEV).flip(0).contiguous()
     q = torch.randn(B, Hq, D, device=DEV, generator=gen).bfloat16()
     out = torch.zeros(B, Hq, D, device=DEV, dtype=torch.bfloat16)
-    ws = torch.empty(B * Hq * 4 * (D + 2), device=DEV, dtype=torch.float32)
+    ws = torch.zeros(B * Hq * 8 * (D + 2), device=DEV, dtype=torch.float32)
     ops.decode_attention(q, cache, bt, slots, seq, out, num_kv_heads=Hkv, max_pages=maxb, workspace=ws, num_sms=sms)
     torch.cuda.synchronize()
     for b in range(B):
@@ -134,7 +134,7 @@ def test_decode_attention_stale_nan_tail():
     slots = torch.arange(4, dtype=torch.int32, device=DEV)
     q = torch.randn(4, Hq, D, device=DEV, generator=gen).bfloat16()
     out = torch.empty(4, Hq, D, device=DEV, dtype=torch.bfloat16)
-    ws = torch.empty(4 * Hq * 1 * (D + 2), device=DEV, dtype=torch.float32)
+    ws = torch.zeros(4 * Hq * 2 * (D + 2), device=DEV, dtype=torch.float32)
     ops.decode_attention(q, cache, bt, slots, seq, out, num_kv_heads=Hkv, max_pages=16, workspace=ws)
     torch.cuda.synchronize()
     for b in range(4):
