@@ -342,6 +342,10 @@ int decode_attention_launch(const void* q, long long q_tok_stride, const void* c
     if (chunk_pages < 8) chunk_pages = 8;
     if (chunk_pages > max_pages) chunk_pages = max_pages;
   }
+  // splitting is an optimisation: without room for the partials, keep whole sequences
+  if ((size_t)B * Hq * ((max_pages + chunk_pages - 1) / chunk_pages) * (kD + 2) * sizeof(float) > ws_bytes ||
+      workspace == nullptr)
+    chunk_pages = max_pages;
   const int splits = (max_pages + chunk_pages - 1) / chunk_pages;  // work items per (sequence, kv head)
   DecArgs a{};
   a.q = reinterpret_cast<const __nv_bfloat16*>(q);
