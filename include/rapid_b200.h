@@ -40,7 +40,9 @@ int rb_debug_gemm_pair_mode(int mode);
  *   Y[t,o] = sum_k X[t,k] W[o,k] (+bias[o]) (+R[t,o])
  * Replaces the compute term of prefill_time (pkg/src/pdsim/costmodel.py:104)
  * and the weight-streaming term of decode_time (costmodel.py:130).
- * mode: 0 auto, 1 token-major tiles (prefill), 2 swap-AB (decode, T<=256).
+ * mode: 0 auto, 1 token-major tiles (prefill), 2 swap-AB (decode, T<=256);
+ * | 4 = fused SwiGLU epilogue: W rows in [gate x16 | up x16] blocks,
+ * Y[t, f] = silu(gate_f) * up_f with O/2 output columns (no bias / R).
  * num_sms: SMs of the partition the stream runs on (persistent grid size).
  * workspace/counters: split-K scratch (fp32) and zeroed int32 tile counters;
  * may be NULL (no split-K). R may alias Y (in-place residual add). */
@@ -112,7 +114,7 @@ typedef struct {
   const void* const* bqkv;  /* [layers] or NULL (Qwen2 bias) */
   const void* const* wo;
   const void* const* ln2;
-  const void* const* wgu;   /* [layers] fused gate|up, [2I, H] */
+  const void* const* wgu;   /* [layers] gate|up rows interleaved in 16-row blocks, [2I, H] */
   const void* const* wd;
   void* kv_cache;           /* layer 0 of [L][num_blocks][2][Hkv][16][D] */
   size_t kv_layer_stride_bytes;

@@ -332,12 +332,12 @@ int decode_attention_launch(const void* q, long long q_tok_stride, const void* c
   if (max_pages < 1) max_pages = 1;
   if (num_sms <= 0) num_sms = 148;
   // Work-item size: whole sequences when (B x Hkv) already gives every warp of the
-  // partition ~2 items (no partials, no combine pass); otherwise cut sequences into
+  // partition at least one item (no partials, no combine pass); otherwise cut sequences into
   // chunks so there are ~4 items per warp (load balance for long contexts / small B).
   const long long warps = (long long)num_sms * kWarps;
   const long long seqs = (long long)B * Hkv;
   int chunk_pages = max_pages;
-  if (seqs < 2 * warps) {
+  if (seqs < warps) {
     chunk_pages = (int)((max_pages * seqs + 4 * warps - 1) / (4 * warps));
     if (chunk_pages < 8) chunk_pages = 8;
     if (chunk_pages > max_pages) chunk_pages = max_pages;

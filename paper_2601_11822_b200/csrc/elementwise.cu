@@ -166,6 +166,38 @@ int silu_mul_launch(const void* gu, long long ld_gu, void* y, long long ldy, int
   return e == cudaSuccess ? 0 : set_cuda_error("silu_mul launch", e);
 }
 
+// Same for gate|up columns interleaved in 16-blocks [g x16 | u x16] (the layout the
+// fused-SwiGLU GEMM epilogue expects); used where the GEMM runs unfused (decode).
+__global__ void silu_mul_il_kernel(const __nv_bfloat16* __restrict__ gu, long long ld_gu,
+                                   __nv_bfloat16* __restrict__ y, long long ldy, int I) {
+  const int t = blockIdx.y;
+  const int f = (blockIdx.x * blockDim.x + threadIdx.x) * 8;  // 8 features, inside one 16-block
+  if (f >= I) return;
+  const __nv_bfloat16* g = gu + (size_t)t * ld_gu + (size_t)(f >> 4) * 32 + (f & 15);
+  uint4 a = *reinterpret_cast<const uint4*>(g);
+  uint4 b = *reinterpret_cast<const uint4*>(g + 16);
+  const uint32_t av[4] = {a.x, a.y, a.z, a.w};
+  const uint32_t bv[4] = {b.x, b.y, b.z, b.w};
+  uint32_t ov[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float2 x = unpack_bf16x2(av[j]);
+    float2 u = unpack_bf16x2(bv[j]);
+    ov[j] = pack_bf16x2(x.x / (1.f + __expf(-x.x)) * u.x, x.y / (1.f + __expf(-x.y)) * u.y);
+  }
+  *reinterpret_cast<uint4*>(y + (size_t)t * ldy + f) = make_uint4(ov[0], ov[1], ov[2], ov[3]);
+}
+
+int silu_mul_interleaved_launch(const void* gu, long long ld_gu, void* y, long long ldy, int T, int I,
+                                cudaStream_t st) {
+  if (T <= 0) return 0;
+  if (I % 16) return set_error("silu_mul_interleaved: I must be a multiple of 16");
+  dim3 grid((I / 8 + 255) / 256, T);
+  silu_mul_il_kernel<<<grid, 256, 0, st>>>((const __nv_bfloat16*)gu, ld_gu, (__nv_bfloat16*)y, ldy, I);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : set_cuda_error("silu_mul_interleaved launch", e);
+}
+
 // ------------------------------------------------------------------ embedding gather
 // ids come either from `ids` directly or, when `slot_of_row` is given, from
 // the per-slot device state last_tok[slot] (decode: the previous step's

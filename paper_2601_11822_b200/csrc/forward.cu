@@ -26,7 +26,8 @@ int rmsnorm_launch(const void* x, long long ldx, const void* w, void* y, long lo
 int rope_cache_launch(const void* qkv, long long ld_qkv, const int* pos, const int* tok_slot, const int* bt,
                       int bt_stride, const float* cos_sin, void* q_out, long long ld_q, void* cache_layer, int T,
                       int Hq, int Hkv, int D, cudaStream_t st);
-int silu_mul_launch(const void* gu, long long ld_gu, void* y, long long ldy, int T, int I, cudaStream_t st);
+int silu_mul_interleaved_launch(const void* gu, long long ld_gu, void* y, long long ldy, int T, int I,
+                                cudaStream_t st);
 int embed_launch(const int* ids, const int* slot_of_row, const int* last_tok, const void* table, void* y, int T, int H,
                  int* ids_out, cudaStream_t st);
 int argmax_launch(const void* logits, long long ld, int T, int V, int* out, const int* slot_of_row, int* last_tok,
@@ -55,7 +56,6 @@ extern "C" int rb_decoder_forward(const rb_model_t* m, const rb_workspace_t* w, 
   char* qkv = static_cast<char*>(w->qkv);
   char* q = static_cast<char*>(w->q);
   char* attn = static_cast<char*>(w->attn);
-  char* gu = static_cast<char*>(w->gu);
   char* act = static_cast<char*>(w->act);
   const int sms = b->num_sms;
   // ---- embedding: decode rows from device slot state, prefill rows from ids[]
@@ -85,9 +85,17 @@ extern "C" int rb_decoder_forward(const rb_model_t* m, const rb_workspace_t* w, 
     RB_TRY(gemm_bf16_launch(attn, m->wo[l], x, nullptr, x, T, H, Hq * D, Hq * D, Hq * D, H, 0, sms, w->gemm_ws,
                             w->gemm_ws_bytes, w->gemm_counters, w->gemm_counters_len, st));
     RB_TRY(rmsnorm_launch(x, H, m->ln2[l], h, H, T, H, m->rms_eps, st));
-    RB_TRY(gemm_bf16_launch(h, m->wgu[l], gu, nullptr, nullptr, T, 2 * I, H, H, H, 2 * I, 0, sms, w->gemm_ws,
-                            w->gemm_ws_bytes, w->gemm_counters, w->gemm_counters_len, st));
-    RB_TRY(silu_mul_launch(gu, 2 * I, act, I, T, I, st));
+    // gate|up (rows interleaved in 16-blocks): token-major tiles fuse the SwiGLU into the
+    // GEMM epilogue; swap-AB (decode) tiles measured faster with the separate kernel.
+    if (T > 256) {
+      RB_TRY(gemm_bf16_launch(h, m->wgu[l], act, nullptr, nullptr, T, 2 * I, H, H, H, I, 4, sms, w->gemm_ws,
+                              w->gemm_ws_bytes, w->gemm_counters, w->gemm_counters_len, st));
+    } else {
+      char* gu = static_cast<char*>(w->gu);
+      RB_TRY(gemm_bf16_launch(h, m->wgu[l], gu, nullptr, nullptr, T, 2 * I, H, H, H, 2 * I, 0, sms, w->gemm_ws,
+                              w->gemm_ws_bytes, w->gemm_counters, w->gemm_counters_len, st));
+      RB_TRY(silu_mul_interleaved_launch(gu, 2 * I, act, I, T, I, st));
+    }
     RB_TRY(gemm_bf16_launch(act, m->wd[l], x, nullptr, x, T, H, I, I, I, H, 0, sms, w->gemm_ws, w->gemm_ws_bytes,
                             w->gemm_counters, w->gemm_counters_len, st));
   }

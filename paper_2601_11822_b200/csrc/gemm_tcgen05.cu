@@ -47,6 +47,7 @@ struct GemmArgs {
   int BN, stages;
   int M_valid, N_valid;  // extents in MMA space
   int swap;              // 1: MMA-M = features (output columns), MMA-N = tokens (output rows)
+  int glu;               // 1: W rows are [gate x16 | up x16] blocks; Y = silu(gate) * up, width O/2
   long long ldy;
   __nv_bfloat16* out;
   const __nv_bfloat16* residual;
@@ -138,6 +139,57 @@ __device__ __forceinline__ void epi_block(const GemmArgs& g, __nv_bfloat16* stg,
         if (g.residual) y += __bfloat162float(g.residual[(long long)row * g.ldy + col + j]);
         dst[j] = __float2bfloat16_rn(y);
       }
+    }
+  }
+  __syncwarp();
+}
+
+// SwiGLU epilogue: the 32 accumulator columns (normal) / rows (swap) of a block are
+// [gate f..f+15 | up f..f+15] for 16 output features f = (block start) / 2.
+__device__ __forceinline__ float silu_mul_f(float gt, float up) { return gt / (1.f + __expf(-gt)) * up; }
+
+__device__ __forceinline__ void epi_block_glu(const GemmArgs& g, __nv_bfloat16* stg, int lane, int m0, int n0,
+                                              const uint32_t (&v)[32]) {
+  if (!g.swap) {
+    // row m0+lane; features n0/2 .. n0/2+15
+    const int row = m0 + lane;
+    const int f0 = n0 >> 1;
+    const int fv = g.N_valid >> 1;
+    if (row < g.M_valid && f0 < fv) {
+      float a[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) a[j] = silu_mul_f(__uint_as_float(v[j]), __uint_as_float(v[16 + j]));
+      __nv_bfloat16* dst = g.out + (long long)row * g.ldy + f0;
+      if (f0 + 16 <= fv) {
+        reinterpret_cast<uint4*>(dst)[0] = make_uint4(pack_bf16x2(a[0], a[1]), pack_bf16x2(a[2], a[3]),
+                                                      pack_bf16x2(a[4], a[5]), pack_bf16x2(a[6], a[7]));
+        reinterpret_cast<uint4*>(dst)[1] = make_uint4(pack_bf16x2(a[8], a[9]), pack_bf16x2(a[10], a[11]),
+                                                      pack_bf16x2(a[12], a[13]), pack_bf16x2(a[14], a[15]));
+      } else {
+        for (int j = 0; j < 16 && f0 + j < fv; ++j) dst[j] = __float2bfloat16_rn(a[j]);
+      }
+    }
+    return;
+  }
+  // swap: lane l < 16 holds gate of feature m0/2 + l, lane l + 16 its up; columns = tokens n0..n0+31
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float up = __shfl_down_sync(0xffffffffu, __uint_as_float(v[j]), 16);
+    if (lane < 16) stg[j * kStgStride + lane] = __float2bfloat16_rn(silu_mul_f(__uint_as_float(v[j]), up));
+  }
+  __syncwarp();
+  const int f0 = m0 >> 1;
+  const int fv = g.M_valid >> 1;
+  // 32 token rows x 16 features: lane -> (row lane, 2 x 16 B)
+  const int row = n0 + lane;
+  if (row < g.N_valid && f0 < fv) {
+    __nv_bfloat16* dst = g.out + (long long)row * g.ldy + f0;
+    const uint4* src = reinterpret_cast<const uint4*>(stg + lane * kStgStride);
+    if (f0 + 16 <= fv) {
+      reinterpret_cast<uint4*>(dst)[0] = src[0];
+      reinterpret_cast<uint4*>(dst)[1] = src[1];
+    } else {
+      for (int j = 0; j < 16 && f0 + j < fv; ++j) dst[j] = stg[lane * kStgStride + j];
     }
   }
   __syncwarp();
@@ -299,7 +351,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t v[32];
             tmem_ld_32x32b_x32(tbase + c, v);
             tmem_ld_wait();
-            if (nt * BN + c < g.N_valid) epi_block(g, stg, lane, m0, nt * BN + c, v);
+            if (nt * BN + c < g.N_valid) {
+              if (g.glu) epi_block_glu(g, stg, lane, m0, nt * BN + c, v);
+              else epi_block(g, stg, lane, m0, nt * BN + c, v);
+            }
           }
         }
         release_acc();
@@ -355,7 +410,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               uint32_t v[32];
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(acc_v[j]);
-              if (nt * BN + c * 32 < g.N_valid) epi_block(g, stg, lane, m0, nt * BN + c * 32, v);
+              if (nt * BN + c * 32 < g.N_valid) {
+                if (g.glu) epi_block_glu(g, stg, lane, m0, nt * BN + c * 32, v);
+                else epi_block(g, stg, lane, m0, nt * BN + c * 32, v);
+              }
             }
           }
         }
@@ -403,6 +461,10 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
   if (ldy % 8 || reinterpret_cast<uintptr_t>(Y) % 16 || (residual && reinterpret_cast<uintptr_t>(residual) % 16) ||
       (bias && reinterpret_cast<uintptr_t>(bias) % 16))
     return set_error("gemm: Y/residual/bias must be 16-byte aligned with ldy % 8 == 0");
+  const int glu = (mode & 4) ? 1 : 0;  // flag bit: fused SwiGLU epilogue
+  mode &= 3;
+  if (glu && (O % 32 != 0 || bias != nullptr || residual != nullptr))
+    return set_error("gemm: SwiGLU epilogue needs O % 32 == 0 and no bias / residual");
   if (mode == 0) mode = (T <= 256) ? 2 : 1;
   const bool swap = (mode == 2);
   if (num_sms <= 0) num_sms = 148;
@@ -463,6 +525,7 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
   g.M_valid = M;
   g.N_valid = N;
   g.swap = swap ? 1 : 0;
+  g.glu = glu;
   g.ldy = ldy;
   g.out = reinterpret_cast<__nv_bfloat16*>(Y);
   g.residual = reinterpret_cast<const __nv_bfloat16*>(residual);

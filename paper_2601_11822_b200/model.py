@@ -7,7 +7,8 @@ replay). Every op goes through the C ABI (ops.py -> librapid_b200.so).
 
 HBM layout:
   * weights: bf16, K-contiguous [out, in]; QKV fused [(Hq+2Hkv)*D, H];
-    gate/up fused [2I, H] (gate rows first)
+    gate/up fused [2I, H], rows interleaved in 16-blocks [g x16 | u x16] so the
+    GEMM epilogue emits silu(gate) * up directly
   * KV cache: one tensor [L][num_blocks][2][Hkv][16][D] bf16 — shared by the
     prefill and decode streams; no KV ever moves between phases
   * block table: int32 [num_slots][max_blocks]; a request owns one slot row
@@ -28,6 +29,14 @@ from paper_2601_11822_b200 import ops
 from paper_2601_11822_b200.specs import ArchConfig
 
 PAGE = 16
+GLU_BLOCK = 16  # gate/up rows are interleaved in blocks of 16 for the fused SwiGLU epilogue
+
+
+def interleave_gate_up(gate: torch.Tensor, up: torch.Tensor) -> torch.Tensor:
+    """[I, H] gate, [I, H] up -> [2I, H] rows [g0..g15, u0..u15, g16..g31, u16..u31, ...]."""
+    I, H = gate.shape
+    return torch.stack([gate.view(I // GLU_BLOCK, GLU_BLOCK, H), up.view(I // GLU_BLOCK, GLU_BLOCK, H)],
+                       dim=1).reshape(2 * I, H)
 
 
 def rope_inv_freq(arch: ArchConfig) -> torch.Tensor:
@@ -108,7 +117,8 @@ class DecoderWeights:
             if arch.qkv_bias:
                 b = t(torch.cat([state[p + "bq"], state[p + "bk"], state[p + "bv"]], 0))
             layers.append(LayerWeights(t(state[p + "ln1"]), t(wqkv), b, t(state[p + "o"]), t(state[p + "ln2"]),
-                                       t(torch.cat([state[p + "gate"], state[p + "up"]], 0)), t(state[p + "down"])))
+                                       t(interleave_gate_up(state[p + "gate"], state[p + "up"])),
+                                       t(state[p + "down"])))
         lm = state.get("lm_head", state["embed"])
         return cls(arch, t(state["embed"]), layers, t(state["norm"]), t(lm))
 

@@ -68,6 +68,27 @@ def test_linear_swap_ab(T, O, K, scratch):
     assert rel_l2(y2, ref) < 1e-2
 
 
+@pytest.mark.parametrize("T,mode", [(1, 2), (37, 2), (200, 2), (300, 1), (1023, 1)])
+@pytest.mark.parametrize("I", [1024, 3584])
+def test_linear_fused_swiglu(T, mode, I, scratch):
+    """mode | 4: gate/up rows interleaved in 16-blocks, epilogue emits silu(gate) * up."""
+    from paper_2601_11822_b200.model import interleave_gate_up
+
+    g = torch.Generator(device=DEV).manual_seed(T + I)
+    K = 1024
+    x = torch.randn(T, K, device=DEV, generator=g).bfloat16()
+    gate = (torch.randn(I, K, device=DEV, generator=g) * 0.05).bfloat16()
+    up = (torch.randn(I, K, device=DEV, generator=g) * 0.05).bfloat16()
+    w = interleave_gate_up(gate, up).contiguous()
+    y = torch.empty(T, I, device=DEV, dtype=torch.bfloat16)
+    ops.load().rb_gemm_bf16(x.data_ptr(), w.data_ptr(), y.data_ptr(), None, None, T, 2 * I, K, K, K, I, mode | 4, 148,
+                            scratch.ws.data_ptr(), scratch.ws_bytes, scratch.counters.data_ptr(),
+                            scratch.counters.numel(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.silu(x.float() @ gate.float().T) * (x.float() @ up.float().T)
+    assert rel_l2(y, ref) < 1e-2
+
+
 def _make_cache(nb, Hkv, D, gen):
     return (torch.randn(nb, 2, Hkv, 16, D, device=DEV, generator=gen) * 0.5).bfloat16()
 
