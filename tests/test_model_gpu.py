@@ -163,6 +163,44 @@ def test_rapid_realtime_end_to_end_matches_oracle(tiny):
     ex.close()
 
 
+def test_rapid_preemption_recompute_on_gpu(tiny):
+    """A KV pool too small for the batch forces RAPID to preempt decoders
+    (rapid.py:221-246); the executor re-prefills prompt + y1..y_{d-1} and resumes
+    with y_d. Every token must still pass the oracle check."""
+    from paper_2601_11822_b200.arm import CostParams
+    from paper_2601_11822_b200.engines.rapid import RapidEngine
+    from paper_2601_11822_b200.executor_b200 import B200Executor
+    from paper_2601_11822_b200.harness import run_items
+    from paper_2601_11822_b200.slo import SloSpec
+    from paper_2601_11822_b200.specs import b200_spec
+    from paper_2601_11822_b200.traffic import WorkloadItem, prompt_token_ids
+
+    arch, st, orc, w = tiny
+    # 10 requests arriving together, 40-token prompts, 40 outputs: 5 pages each at the end
+    items = [WorkloadItem(1000 + 10 * i, 40, 40) for i in range(10)]
+    ex = B200Executor(arch, weights=w, max_batch=16, chunk_tokens=64, num_blocks=36, max_context=256,
+                      num_slots=32, static_decode_sms=72)
+    ex.warmup()
+    model = arch.model_spec()
+    slo = SloSpec(itl_slo_us=50_000)
+    res = run_items("rapid", items, model, b200_spec(), CostParams(), slo,
+                    engine_factory=lambda: RapidEngine(model, b200_spec(), CostParams(), slo, chunk_tokens=64,
+                                                       max_batch=16, executor=ex))
+    reqs = res.engine.requests
+    assert sum(r.preemptions for r in reqs) >= 1, "pool did not force a preemption"
+    exact = flips = 0
+    for r in reqs:
+        assert r.state.value == "finished"
+        prompt = prompt_token_ids(r.id, r.prompt_tokens, arch.vocab)
+        assert len(ex.generated[r.id]) == r.output_tokens
+        e, f = teacher_forced_check(orc, prompt, ex.generated[r.id])
+        exact += e
+        flips += f
+    print(f"preemption run: {sum(r.preemptions for r in reqs)} preemptions, {exact} exact, {flips} flips")
+    assert flips <= 0.1 * (exact + flips), (exact, flips)
+    ex.close()
+
+
 def test_hybrid_realtime_end_to_end_matches_oracle(tiny):
     """Same-engine hybrid batching (fused decode rows + prefill chunk per
     iteration) on the B200: invariants hold, first tokens come from the chunk
