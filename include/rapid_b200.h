@@ -73,6 +73,13 @@ int rb_prefill_attention(const void* q, long long q_tok_stride, const void* cach
                          int T, int start, int Hq, int Hkv, int head_dim, void* out, long long out_tok_stride,
                          float scale, void* stream);
 
+/* K2 on tcgen05: same contract as rb_prefill_attention, computed with
+ * tcgen05.mma (S = QK^T and O = PV accumulate in TMEM), Q and paged K/V fed by
+ * TMA. num_blocks = pages in the cache layer (TMA extent). */
+int rb_prefill_attention_tc(const void* q, long long q_tok_stride, const void* cache_layer,
+                            const int* block_table_row, int T, int start, int Hq, int Hkv, int head_dim, void* out,
+                            long long out_tok_stride, float scale, int num_blocks, void* stream);
+
 /* K5 — RoPE on q,k + paged KV write of k,v for T rows (pos[t] < 0 skips).
  * Replaces the KV-write term kv_cache_bytes(model, tokens) of prefill_time
  * (costmodel.py:105) and kv_cache_bytes(model, batch) of decode_time (:132).

@@ -1,0 +1,377 @@
+// K2 (tcgen05): prefill causal flash-attention over the paged KV cache on
+// 5th-gen tensor cores, TMA-fed.
+//
+// Realizes the attention share of prefill_time's compute term (reference
+// pkg/src/pdsim/costmodel.py:104) for one prefill chunk (rapid.py:313): queries
+// at positions start..start+T-1 of one request attend to keys [0, start+T) of its
+// paged cache (prefix U chunk; the chunk's K,V were written by the RoPE/cache
+// kernel that precedes this one), causal mask shifted by `start`.
+//
+// CTA = 128 query positions x 1 query head, 192 threads:
+//   w0      TMA producer: Q once (3D map over [T][Hq][128]), then 64-key K/V
+//           tiles = 4 pages x {K lo, K hi, V lo, V hi} boxes {64 x 16} (2D map
+//           over the cache layer) into a 3-stage ring, 128B swizzle.
+//   w1      TMEM owner + single-thread MMA issuer:
+//             S_j = Q K_j^T   (M=128, N=64,  K=128; A,B K-major)     -> TMEM S[j%2]
+//             O_j = P_j V_j   (M=128, N=128, K=64;  B = V MN-major)  -> TMEM O[j%2]
+//           S_{j+1} is issued before O_j so QK^T overlaps the softmax.
+//   w2..w5  softmax (thread = query row = TMEM lane): S row -> mask, running
+//           max/sum (exp2) -> P row (bf16) into smem in the UMMA K-major
+//           layout -> after O_j lands, o = o*alpha + O_j in registers.
+// Output row = o / l, written straight from registers (256 B per row).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cfloat>
+#include "ptx.cuh"
+#include "rb_common.h"
+
+namespace rb {
+
+namespace fa {
+constexpr int kD = 128;
+constexpr int kBMq = 128;                  // query rows per CTA
+constexpr int kBN = 64;                    // keys per tile
+constexpr int kPage = 16;
+constexpr int kStages = 3;
+constexpr int kQBytes = 2 * kBMq * 128;    // two 64-dim halves, 16 KB each
+constexpr int kKVHalf = kBN * 128;         // 8 KB: 64 keys x 64 dims
+constexpr int kKVStage = 4 * kKVHalf;      // K lo, K hi, V lo, V hi = 32 KB
+constexpr int kPBytes = kBMq * kBN * 2;    // 16 KB
+constexpr int kThreads = 192;
+constexpr int kTmemCols = 512;             // S[2] x 64 + O[2] x 128 = 384 -> 512
+constexpr uint32_t kSCol = 0, kOCol = 128;
+}  // namespace fa
+
+// K-major SW128 descriptor with explicit SBO (atoms of 8 rows x 128 B)
+__device__ __forceinline__ uint64_t sdesc_kmajor(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+// MN-major SW128 descriptor: 64-element MN blocks LBO apart, 8-row K groups SBO=1024 apart
+__device__ __forceinline__ uint64_t sdesc_mnmajor(uint32_t saddr, uint32_t lbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst_smem, const void* tmap, uint64_t* bar, int32_t x, int32_t y,
+                                            int32_t z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst_smem)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld_x32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  tmem_ld_32x32b_x32(taddr, r);
+  tmem_ld_wait();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__global__ void __launch_bounds__(fa::kThreads, 1)
+    prefill_attn_tc_kernel(const __grid_constant__ CUtensorMap q_map, const __grid_constant__ CUtensorMap kv_map,
+                           const int* __restrict__ bt, int T, int start, int Hq, int Hkv,
+                           __nv_bfloat16* __restrict__ out, long long out_tok_stride, float scale_log2) {
+  using namespace fa;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sKV = sQ + kQBytes;
+  uint8_t* sP = sKV + kStages * kKVStage;  // [2][16 KB]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * kPBytes);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = kv_full + kStages;
+  uint64_t* s_full = kv_empty + kStages;  // [2]
+  uint64_t* s_free = s_full + 2;
+  uint64_t* p_full = s_free + 2;
+  uint64_t* p_free = p_full + 2;
+  uint64_t* o_full = p_free + 2;
+  uint64_t* o_free = o_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nqb = (T + kBMq - 1) / kBMq;
+  const int qb = nqb - 1 - (int)blockIdx.x;  // latest (heaviest) query blocks first
+  const int hq = blockIdx.y;
+  const int hk = hq / (Hq / Hkv);
+  const int q0 = qb * kBMq;
+  const int kv_end = start + min(T, q0 + kBMq);
+  const int n_tiles = (kv_end + kBN - 1) / kBN;
+  const int last_page = (start + T - 1) / kPage;  // highest page index this chunk may touch
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&s_free[b], 4);
+      mbar_init(&p_full[b], 4);
+      mbar_init(&p_free[b], 1);
+      mbar_init(&o_full[b], 1);
+      mbar_init(&o_free[b], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ================= TMA producer =================
+      tma_prefetch_desc(&q_map);
+      tma_prefetch_desc(&kv_map);
+      mbar_arrive_expect_tx(q_full, kQBytes);
+      tma_load_3d(sQ, &q_map, q_full, 0, hq, q0);
+      tma_load_3d(sQ + kQBytes / 2, &q_map, q_full, 64, hq, q0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int j = 0; j < n_tiles; ++j) {
+        mbar_wait(&kv_empty[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&kv_full[stage], kKVStage);
+        uint8_t* dst = sKV + (size_t)stage * kKVStage;
+        for (int pg = 0; pg < kBN / kPage; ++pg) {
+          int pidx = j * (kBN / kPage) + pg;
+          if (pidx > last_page) pidx = last_page;  // past the chunk: finite data, masked in softmax
+          const int page = bt[pidx];
+          const int rowK = ((page * 2 + 0) * Hkv + hk) * kPage;
+          const int rowV = ((page * 2 + 1) * Hkv + hk) * kPage;
+          tma_load_2d(dst + 0 * kKVHalf + pg * 2048, &kv_map, &kv_full[stage], 0, rowK, kEvictNormal);
+          tma_load_2d(dst + 1 * kKVHalf + pg * 2048, &kv_map, &kv_full[stage], 64, rowK, kEvictNormal);
+          tma_load_2d(dst + 2 * kKVHalf + pg * 2048, &kv_map, &kv_full[stage], 0, rowV, kEvictNormal);
+          tma_load_2d(dst + 3 * kKVHalf + pg * 2048, &kv_map, &kv_full[stage], 64, rowV, kEvictNormal);
+        }
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ================= MMA issuer =================
+      const uint32_t idesc_s = make_idesc_bf16(kBMq, kBN);
+      const uint32_t idesc_o = make_idesc_bf16(kBMq, kD) | (1u << 16);  // B (V) MN-major
+      const uint32_t qa = smem_u32(sQ);
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      auto issue_s = [&](int j) {
+        const int st = j % kStages;
+        const uint32_t ph = (uint32_t)((j / kStages) & 1);
+        const int b = j & 1;
+        mbar_wait(&kv_full[st], ph);
+        mbar_wait(&s_free[b], (uint32_t)(((j >> 1) & 1) ^ 1));
+        tc_fence_after();
+        const uint32_t kb = smem_u32(sKV + (size_t)st * kKVStage);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (uint32_t)((kk >> 2) * 0 + (kk & 3) * 32);
+          const uint64_t ad = sdesc_kmajor(qa + (kk >> 2) * (kQBytes / 2) + off);
+          const uint64_t bd = sdesc_kmajor(kb + (kk >> 2) * kKVHalf + off);
+          umma_bf16(tmem + kSCol + (uint32_t)b * kBN, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[b]);
+      };
+      if (n_tiles > 0) issue_s(0);
+      for (int j = 0; j < n_tiles; ++j) {
+        if (j + 1 < n_tiles) issue_s(j + 1);
+        const int st = j % kStages;
+        const int b = j & 1;
+        const uint32_t ph2 = (uint32_t)((j >> 1) & 1);
+        mbar_wait(&p_full[b], ph2);
+        mbar_wait(&o_free[b], ph2 ^ 1);
+        tc_fence_after();
+        const uint32_t pa = smem_u32(sP + (size_t)b * kPBytes);
+        const uint32_t vb = smem_u32(sKV + (size_t)st * kKVStage + 2 * kKVHalf);
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk) {
+          const uint64_t ad = sdesc_kmajor(pa + kk * 32);
+          const uint64_t bd = sdesc_mnmajor(vb + kk * 2048, kKVHalf);
+          umma_bf16(tmem + kOCol + (uint32_t)b * kD, ad, bd, idesc_o, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&o_full[b]);
+        umma_commit(&p_free[b]);
+        umma_commit(&kv_empty[st]);
+      }
+    }
+  } else {
+    // ================= softmax warps: thread = query row =================
+    const int qd = warp & 3;
+    const int row = qd * 32 + lane;
+    const int qpos = start + q0 + row;
+    const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
+    float o[kD];
+#pragma unroll
+    for (int i = 0; i < kD; ++i) o[i] = 0.f;
+    float m = -FLT_MAX, l = 0.f;
+    float alpha_prev = 1.f;
+    // o <- o * alpha_jj + O_jj, where alpha_jj rescales o (relative to m_{jj-1}) to m_jj
+    auto fold_o = [&](int jj, float a) {
+      const int bb = jj & 1;
+      mbar_wait(&o_full[bb], (uint32_t)((jj >> 1) & 1));
+      tc_fence_after();
+#pragma unroll
+      for (int cc = 0; cc < kD / 32; ++cc) {
+        float t[32];
+        tmem_ld_x32(tmem + lane_off + kOCol + (uint32_t)bb * kD + cc * 32, t);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[cc * 32 + i] = o[cc * 32 + i] * a + t[i];
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_free[bb]);
+    };
+    for (int j = 0; j < n_tiles; ++j) {
+      const int b = j & 1;
+      const uint32_t ph2 = (uint32_t)((j >> 1) & 1);
+      mbar_wait(&s_full[b], ph2);
+      tc_fence_after();
+      float s[kBN];
+      {
+        float t0[32], t1[32];
+        tmem_ld_x32(tmem + lane_off + kSCol + (uint32_t)b * kBN, t0);
+        tmem_ld_x32(tmem + lane_off + kSCol + (uint32_t)b * kBN + 32, t1);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          s[i] = t0[i];
+          s[32 + i] = t1[i];
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[b]);
+      const int kbase = j * kBN;
+      float mx = -FLT_MAX;
+#pragma unroll
+      for (int i = 0; i < kBN; ++i) {
+        const int kp = kbase + i;
+        const float v = (kp > qpos || kp >= kv_end) ? -FLT_MAX : s[i] * scale_log2;
+        s[i] = v;
+        mx = fmaxf(mx, v);
+      }
+      const float mn = fmaxf(m, mx);
+      const float alpha = (mn == -FLT_MAX) ? 1.f : exp2f(m - mn);
+      m = mn;
+      float ps = 0.f;
+#pragma unroll
+      for (int i = 0; i < kBN; ++i) {
+        const float p = (s[i] == -FLT_MAX) ? 0.f : exp2f(s[i] - mn);
+        s[i] = p;
+        ps += p;
+      }
+      l = l * alpha + ps;
+      // P row -> smem (K-major SW128: row r at (r/8)*1024 + (r%8)*128, 16-B chunk c at c ^ (r%8))
+      mbar_wait(&p_free[b], ph2 ^ 1);
+      uint8_t* prow = sP + (size_t)b * kPBytes + (row >> 3) * 1024 + (row & 7) * 128;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint4 v = make_uint4(pack_bf16x2(s[8 * c + 0], s[8 * c + 1]), pack_bf16x2(s[8 * c + 2], s[8 * c + 3]),
+                                   pack_bf16x2(s[8 * c + 4], s[8 * c + 5]), pack_bf16x2(s[8 * c + 6], s[8 * c + 7]));
+        *reinterpret_cast<uint4*>(prow + ((c ^ (row & 7)) << 4)) = v;
+      }
+      if (kbase + kBN > kv_end) {
+        // keys past the chunk in its last page may never have been written (non-finite
+        // bit patterns); P is 0 there but 0 * NaN would poison the PV MMA -> zero those V rows
+        const int st = j % kStages;
+        uint8_t* vbase = sKV + (size_t)st * kKVStage + 2 * kKVHalf;
+        const int first = max(0, kv_end - kbase);
+        for (int i = row; i < (kBN - first) * 16; i += kBMq) {  // 16 chunks of 16 B per key (2 halves)
+          const int key = first + (i >> 4);
+          const int ch = i & 15;
+          uint8_t* p = vbase + (ch >> 3) * kKVHalf + (key >> 3) * 1024 + (key & 7) * 128 + (ch & 7) * 16;
+          *reinterpret_cast<uint4*>(p) = make_uint4(0u, 0u, 0u, 0u);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[b]);
+      // fold O_{j-1} (computed by the tensor cores while this tile's softmax ran)
+      if (j > 0) fold_o(j - 1, alpha_prev);
+      alpha_prev = alpha;
+    }
+    if (n_tiles > 0) fold_o(n_tiles - 1, alpha_prev);
+    const int trow = q0 + row;
+    if (trow < T) {
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      __nv_bfloat16* dst = out + (size_t)trow * out_tok_stride + (size_t)hq * kD;
+#pragma unroll
+      for (int c = 0; c < kD / 8; ++c) {
+        reinterpret_cast<uint4*>(dst)[c] =
+            make_uint4(pack_bf16x2(o[8 * c] * inv, o[8 * c + 1] * inv), pack_bf16x2(o[8 * c + 2] * inv, o[8 * c + 3] * inv),
+                       pack_bf16x2(o[8 * c + 4] * inv, o[8 * c + 5] * inv), pack_bf16x2(o[8 * c + 6] * inv, o[8 * c + 7] * inv));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tmem_dealloc(tmem, kTmemCols);
+  }
+}
+
+typedef CUresult (*PFN_encodeTiled3)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int prefill_attention_tc_launch(const void* q, long long q_tok_stride, const void* cache_layer, const int* bt, int T,
+                                int start, int Hq, int Hkv, int head_dim, void* out, long long out_tok_stride,
+                                float scale, int num_blocks, cudaStream_t st) {
+  using namespace fa;
+  if (T <= 0) return 0;
+  if (head_dim != kD) return set_error("prefill attention (tc): head_dim must be 128");
+  if (Hkv <= 0 || Hq % Hkv != 0) return set_error("prefill attention (tc): bad head counts");
+  if ((q_tok_stride * 2) % 16) return set_error("prefill attention (tc): q token stride must be 16-byte aligned");
+  static PFN_encodeTiled3 enc = nullptr;
+  if (!enc) {
+    enc = reinterpret_cast<PFN_encodeTiled3>(driver_symbol("cuTensorMapEncodeTiled"));
+    if (!enc) return set_error("cuTensorMapEncodeTiled unavailable");
+  }
+  CUtensorMap qmap;
+  {
+    cuuint64_t dims[3] = {(cuuint64_t)kD, (cuuint64_t)Hq, (cuuint64_t)T};
+    cuuint64_t strides[2] = {(cuuint64_t)kD * 2, (cuuint64_t)q_tok_stride * 2};
+    cuuint32_t box[3] = {64, 1, (cuuint32_t)kBMq};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(&qmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(q), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_cu_error("cuTensorMapEncodeTiled(q)", r);
+  }
+  CUtensorMap kvmap;
+  int rc = make_tmap_2d_bf16(&kvmap, cache_layer, kD, (uint64_t)num_blocks * 2 * Hkv * kPage, kD, 64, kPage);
+  if (rc) return rc;
+  const int smem = kQBytes + kStages * kKVStage + 2 * kPBytes + 24 * 8 + 1024 + 64;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(prefill_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return set_cuda_error("prefill attn tc smem attr", e);
+    attr = true;
+  }
+  dim3 grid((T + kBMq - 1) / kBMq, Hq);
+  prefill_attn_tc_kernel<<<grid, kThreads, smem, st>>>(qmap, kvmap, bt, T, start, Hq, Hkv,
+                                                       reinterpret_cast<__nv_bfloat16*>(out), out_tok_stride,
+                                                       scale * 1.4426950408889634f);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error("prefill attn tc launch", e);
+  return 0;
+}
+
+}  // namespace rb

@@ -24,6 +24,9 @@ int argmax_launch(const void* logits, long long ld, int T, int V, int* out, cons
                   const int* row_valid, cudaStream_t st);
 int bt_update_launch(const int* upd, int* block_table, int bt_stride, int max_updates, cudaStream_t st);
 int set_last_tok_launch(int* last_tok, int slot, const int* value_ptr, int value, cudaStream_t st);
+int prefill_attention_tc_launch(const void* q, long long q_tok_stride, const void* cache_layer, const int* bt, int T,
+                                int start, int Hq, int Hkv, int head_dim, void* out, long long out_tok_stride,
+                                float scale, int num_blocks, cudaStream_t st);
 int gemm_set_trace(unsigned long long* buf);
 int gemm_set_pair_mode(int mode);
 }  // namespace rb
@@ -64,6 +67,13 @@ int rb_prefill_attention(const void* q, long long q_tok_stride, const void* cach
                          float scale, void* stream) {
   return rb::prefill_attention_launch(q, q_tok_stride, cache_layer, block_table_row, T, start, Hq, Hkv, head_dim, out,
                                       out_tok_stride, scale, ST(stream));
+}
+
+int rb_prefill_attention_tc(const void* q, long long q_tok_stride, const void* cache_layer,
+                            const int* block_table_row, int T, int start, int Hq, int Hkv, int head_dim, void* out,
+                            long long out_tok_stride, float scale, int num_blocks, void* stream) {
+  return rb::prefill_attention_tc_launch(q, q_tok_stride, cache_layer, block_table_row, T, start, Hq, Hkv, head_dim,
+                                         out, out_tok_stride, scale, num_blocks, ST(stream));
 }
 
 int rb_rope_cache_write(const void* qkv, long long ld_qkv, const int* pos, const int* tok_slot,

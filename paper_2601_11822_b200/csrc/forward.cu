@@ -21,6 +21,9 @@ int decode_attention_launch(const void* q, long long q_tok_stride, const void* c
 int prefill_attention_launch(const void* q, long long q_tok_stride, const void* cache_layer, const int* bt, int T,
                              int start, int Hq, int Hkv, int head_dim, void* out, long long out_tok_stride,
                              float scale, cudaStream_t st);
+int prefill_attention_tc_launch(const void* q, long long q_tok_stride, const void* cache_layer, const int* bt, int T,
+                                int start, int Hq, int Hkv, int head_dim, void* out, long long out_tok_stride,
+                                float scale, int num_blocks, cudaStream_t st);
 int rmsnorm_launch(const void* x, long long ldx, const void* w, void* y, long long ldy, int T, int H, float eps,
                    cudaStream_t st);
 int rope_cache_launch(const void* qkv, long long ld_qkv, const int* pos, const int* tok_slot, const int* bt,
@@ -78,10 +81,10 @@ extern "C" int rb_decoder_forward(const rb_model_t* m, const rb_workspace_t* w, 
                                      (long long)Hq * D, w->attn_ws, w->attn_ws_bytes, nd, Hq, Hkv, D, b->max_pages,
                                      m->attn_scale, m->num_blocks, sms, st));
     if (np > 0)
-      RB_TRY(prefill_attention_launch(q + (size_t)nd * Hq * D * e, (long long)Hq * D, cache,
-                                      m->block_table + (size_t)b->prefill_slot * m->bt_stride, np, b->prefill_start,
-                                      Hq, Hkv, D, attn + (size_t)nd * Hq * D * e, (long long)Hq * D, m->attn_scale,
-                                      st));
+      RB_TRY(prefill_attention_tc_launch(q + (size_t)nd * Hq * D * e, (long long)Hq * D, cache,
+                                         m->block_table + (size_t)b->prefill_slot * m->bt_stride, np,
+                                         b->prefill_start, Hq, Hkv, D, attn + (size_t)nd * Hq * D * e,
+                                         (long long)Hq * D, m->attn_scale, m->num_blocks, st));
     RB_TRY(gemm_bf16_launch(attn, m->wo[l], x, nullptr, x, T, H, Hq * D, Hq * D, Hq * D, H, 0, sms, w->gemm_ws,
                             w->gemm_ws_bytes, w->gemm_counters, w->gemm_counters_len, st));
     RB_TRY(rmsnorm_launch(x, H, m->ln2[l], h, H, T, H, m->rms_eps, st));

@@ -171,7 +171,8 @@ class Runner:
         self.num_slots = num_slots
         self.dummy_slot = num_slots  # padding rows of a decode bucket point here
         self.max_blocks = max_blocks_per_seq
-        self.kv = torch.empty(arch.layers, num_blocks, 2, arch.kv_heads, PAGE, arch.head_dim, dtype=torch.bfloat16,
+        # zeroed once so never-written slots hold finite values (kernels also mask them)
+        self.kv = torch.zeros(arch.layers, num_blocks, 2, arch.kv_heads, PAGE, arch.head_dim, dtype=torch.bfloat16,
                               device=self.device)
         self.block_table = torch.zeros(num_slots + 1, max_blocks_per_seq, dtype=torch.int32, device=self.device)
         self.last_tok = torch.zeros(num_slots + 1, dtype=torch.int32, device=self.device)

@@ -44,6 +44,10 @@ _SIGS = {
         [_vp, _c_ll, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _c_ll, _c_float, _vp],
         _c_int,
     ),
+    "rb_prefill_attention_tc": (
+        [_vp, _c_ll, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _c_ll, _c_float, _c_int, _vp],
+        _c_int,
+    ),
     "rb_rope_cache_write": (
         [_vp, _c_ll, _vp, _vp, _vp, _c_int, _vp, _vp, _c_ll, _vp, _c_int, _c_int, _c_int, _c_int, _vp],
         _c_int,
@@ -220,11 +224,23 @@ def decode_attention(q: torch.Tensor, cache_layer: torch.Tensor, block_table: to
 
 
 def prefill_attention(q: torch.Tensor, cache_layer: torch.Tensor, block_table_row: torch.Tensor, start: int,
-                      out: torch.Tensor, *, num_kv_heads: int, scale: float | None = None, stream=None) -> torch.Tensor:
-    """q, out: [T, Hq, D] for chunk positions start..start+T-1 of one request."""
+                      out: torch.Tensor, *, num_kv_heads: int, scale: float | None = None, impl: str = "tc",
+                      stream=None) -> torch.Tensor:
+    """q, out: [T, Hq, D] for chunk positions start..start+T-1 of one request.
+
+    impl "tc": tcgen05/TMEM/TMA kernel (default); "mma": GQA-packed mma.sync kernel."""
     _need_cuda(q, cache_layer, block_table_row, out)
     T, Hq, D = q.shape
     sc = scale if scale is not None else 1.0 / math.sqrt(D)
+    if impl == "tc":
+        _check(
+            load().rb_prefill_attention_tc(
+                _ptr(q), q.stride(0), _ptr(cache_layer), _ptr(block_table_row), T, start, Hq, num_kv_heads, D,
+                _ptr(out), out.stride(0), sc, cache_layer.shape[0], _stream(stream),
+            ),
+            "rb_prefill_attention_tc",
+        )
+        return out
     _check(
         load().rb_prefill_attention(
             _ptr(q), q.stride(0), _ptr(cache_layer), _ptr(block_table_row), T, start, Hq, num_kv_heads, D, _ptr(out),

@@ -11,6 +11,10 @@ for (T, start, Hq, Hkv) in [(1023, 0, 32, 8), (2048, 0, 32, 8), (2048, 6144, 40,
     bt = torch.arange(nb, dtype=torch.int32, device=dev)
     q = torch.randn(T, Hq, 128, device=dev).bfloat16()
     out = torch.empty_like(q)
-    ms = timeit(lambda: ops.prefill_attention(q, cache, bt, start, out, num_kv_heads=Hkv))
     flops = 4 * Hq * 128 * (T * T / 2 + T * start)
-    print(json.dumps(dict(T=T, start=start, Hq=Hq, Hkv=Hkv, us=round(ms * 1e3, 1), tflops=round(flops / ms / 1e9, 1))))
+    row = dict(T=T, start=start, Hq=Hq, Hkv=Hkv)
+    for impl in ("mma", "tc"):
+        ms = timeit(lambda: ops.prefill_attention(q, cache, bt, start, out, num_kv_heads=Hkv, impl=impl))
+        row[impl + "_us"] = round(ms * 1e3, 1)
+        row[impl + "_tflops"] = round(flops / ms / 1e9, 1)
+    print(json.dumps(row))

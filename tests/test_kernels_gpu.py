@@ -180,20 +180,40 @@ def test_decode_attention_padded_rows():
     assert rel_l2(out[3:4], _ref_attn(q[3:4], k, v)) < 1e-2
 
 
+@pytest.mark.parametrize("impl", ["tc", "mma"])
 @pytest.mark.parametrize("T,start,Hq,Hkv", [(100, 0, 8, 2), (64, 37, 8, 2), (200, 130, 32, 8), (1, 50, 40, 8),
-                                            (257, 0, 8, 1)])
-def test_prefill_attention(T, start, Hq, Hkv):
+                                            (257, 0, 8, 1), (300, 500, 32, 8)])
+def test_prefill_attention(T, start, Hq, Hkv, impl):
     gen = torch.Generator(device=DEV).manual_seed(T + start)
     D, nb = 128, 256
     cache = _make_cache(nb, Hkv, D, gen)
     bt_row = torch.randperm(nb, device=DEV, generator=gen).int()[:64].contiguous()
+    assert (start + T + 15) // 16 <= 64
     q = torch.randn(T, Hq, D, device=DEV, generator=gen).bfloat16()
     out = torch.empty(T, Hq, D, device=DEV, dtype=torch.bfloat16)
-    ops.prefill_attention(q, cache, bt_row, start, out, num_kv_heads=Hkv)
+    ops.prefill_attention(q, cache, bt_row, start, out, num_kv_heads=Hkv, impl=impl)
     torch.cuda.synchronize()
     k, v = _gather_kv(cache, bt_row, start + T)
     ref = _ref_attn(q, k, v, causal_offset=start)
     assert rel_l2(out, ref) < 1e-2
+
+
+@pytest.mark.parametrize("impl", ["tc", "mma"])
+def test_prefill_attention_stale_nan_tail(impl):
+    """Slots after the chunk end in its last page may never have been written."""
+    gen = torch.Generator(device=DEV).manual_seed(99)
+    D, nb, Hq, Hkv, T, start = 128, 64, 32, 8, 70, 25
+    cache = _make_cache(nb, Hkv, D, gen)
+    bt_row = torch.randperm(nb, device=DEV, generator=gen).int()[:16].contiguous()
+    n = start + T
+    cache[int(bt_row[n // 16]), :, :, n % 16:] = float("nan")
+    q = torch.randn(T, Hq, D, device=DEV, generator=gen).bfloat16()
+    out = torch.empty(T, Hq, D, device=DEV, dtype=torch.bfloat16)
+    ops.prefill_attention(q, cache, bt_row, start, out, num_kv_heads=Hkv, impl=impl)
+    torch.cuda.synchronize()
+    k, v = _gather_kv(cache, bt_row, n)
+    assert torch.isfinite(out).all()
+    assert rel_l2(out, _ref_attn(q, k, v, causal_offset=start)) < 1e-2
 
 
 def _cos_sin(max_pos, D, theta=10000.0):
