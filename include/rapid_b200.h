@@ -35,6 +35,9 @@ int rb_device_sm_count(int device, int* out);
 int rb_debug_gemm_trace(unsigned long long* buf);
 /* Debug: GEMM CTA-pair policy, -1 auto (default), 0 force single-CTA, 1 force 2-CTA pairs. */
 int rb_debug_gemm_pair_mode(int mode);
+/* Debug: decode (swap-AB) GEMM schedule, -1 auto (default); else bit0 = two 128-row weight
+ * sub-tiles per activation stage, bit1 = stream-K (else data-parallel whole tiles). */
+int rb_debug_gemm_variant(int v);
 
 /* K1/K4 — bf16 linear layer on tcgen05 tensor cores:
  *   Y[t,o] = sum_k X[t,k] W[o,k] (+bias[o]) (+R[t,o])

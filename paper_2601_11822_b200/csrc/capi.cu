@@ -29,6 +29,7 @@ int prefill_attention_tc_launch(const void* q, long long q_tok_stride, const voi
                                 float scale, int num_blocks, cudaStream_t st);
 int gemm_set_trace(unsigned long long* buf);
 int gemm_set_pair_mode(int mode);
+int gemm_set_variant(int v);
 }  // namespace rb
 
 #define ST(s) reinterpret_cast<cudaStream_t>(s)
@@ -40,6 +41,7 @@ const char* rb_last_error(void) { return rb::last_error(); }
 
 int rb_debug_gemm_trace(unsigned long long* buf) { return rb::gemm_set_trace(buf); }
 int rb_debug_gemm_pair_mode(int mode) { return rb::gemm_set_pair_mode(mode); }
+int rb_debug_gemm_variant(int v) { return rb::gemm_set_variant(v); }
 
 int rb_device_sm_count(int device, int* out) {
   cudaError_t e = cudaDeviceGetAttribute(out, cudaDevAttrMultiProcessorCount, device);

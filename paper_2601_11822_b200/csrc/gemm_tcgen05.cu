@@ -43,8 +43,16 @@ constexpr int kStgBytes = 32 * kStgStride * 2;  // per epilogue warp
 
 struct GemmArgs {
   int m_tiles, n_tiles, num_kb, total_tiles;
-  int splits, kb_per_split, total_units;  // unit = tile * splits + split
+  int streamk;     // 1: stream-K — each cluster owns an equal run of the (tile, k-block) iterations
+  int total_iters; // total_tiles * num_kb
+  int mt;          // A sub-tiles of kBM*kPair rows per tile, sharing one B stage
+  int nacc;        // TMEM accumulator buffers (2: epilogue of segment i overlaps MMAs of i+1)
+  int kacc;        // independent K-interleaved accumulators per buffer (MMA kk -> kk % kacc), summed
+                   // in the epilogue: breaks the serial dependence of skinny (small-N) MMAs
   int BN, stages;
+  int a_blocked;   // A (swap: the weight) stored as [rows/128][num_kb][128][64] contiguous 16 KB blocks
+  int pf_dist;     // k-blocks of A to warm in L2 ahead of the smem ring (0 = off)
+  int dbg;         // debug (kPair 1 only): 1 = skip the MMAs, 2 = skip the TMA loads
   int M_valid, N_valid;  // extents in MMA space
   int swap;              // 1: MMA-M = features (output columns), MMA-N = tokens (output rows)
   int glu;               // 1: W rows are [gate x16 | up x16] blocks; Y = silu(gate) * up, width O/2
@@ -53,8 +61,52 @@ struct GemmArgs {
   const __nv_bfloat16* residual;
   const __nv_bfloat16* bias;
   uint64_t hint_a, hint_b;
-  float* ws;      // split-K partials [tile][cta][split][BN/32][4 warps][8][32 lanes] float4
-  int* counters;  // per (tile, cta), self-resetting
+  float* ws;      // stream-K partials [cluster][rank][mt][BN/32][4 warps][8][32 lanes] float4
+  int* counters;  // per (tile, rank), self-resetting
+};
+
+// Work schedule shared by the producer, MMA and epilogue roles. Data-parallel: whole
+// tiles, strided over clusters. Stream-K: cluster c owns iterations
+// [c*I/G, (c+1)*I/G) of the flattened (tile, k-block) space and walks them from the
+// end, so a tile split between clusters c_first..c_last is reached FIRST by c_first..
+// c_last-1 (their runs end in it: they publish fp32 partials early) and LAST by c_last
+// (its run starts in it): c_last is the finisher. It waits only on lower-numbered
+// clusters, which are dispatched first, so the spin cannot deadlock even when the grid
+// is not fully co-resident; the sum order is fixed (deterministic for a partition size).
+__device__ __forceinline__ int sk_start(const GemmArgs& g, int c, int ncl) {
+  return (int)(((long long)c * g.total_iters) / ncl);
+}
+// first cluster whose run contains iteration x
+__device__ __forceinline__ int sk_owner(const GemmArgs& g, int x, int ncl) {
+  return (int)((((long long)x + 1) * ncl - 1) / g.total_iters);
+}
+struct SegIter {
+  int lo, it;   // stream-K: this cluster's run [lo, it), walked from the END (descending)
+  int t, step;  // data-parallel cursor
+  __device__ __forceinline__ SegIter(const GemmArgs& g, int cid, int ncl) {
+    lo = sk_start(g, cid, ncl);
+    it = sk_start(g, cid + 1, ncl);
+    t = cid;
+    step = ncl;
+  }
+  __device__ __forceinline__ bool next(const GemmArgs& g, int& tile, int& kb0, int& kb1) {
+    if (g.streamk) {
+      if (it <= lo) return false;
+      tile = (it - 1) / g.num_kb;
+      const int base = tile * g.num_kb;
+      const int seg_lo = max(lo, base);
+      kb0 = seg_lo - base;
+      kb1 = it - base;
+      it = seg_lo;
+      return true;
+    }
+    if (t >= g.total_tiles) return false;
+    tile = t;
+    kb0 = 0;
+    kb1 = g.num_kb;
+    t += step;
+    return true;
+  }
 };
 
 // Optional timeline trace (debug): per CTA 8 globaltimer stamps.
@@ -64,9 +116,11 @@ __device__ __forceinline__ unsigned long long gtime() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-#define TRACE(slot)                                                     \
-  do {                                                                  \
-    if (g_gemm_trace) g_gemm_trace[blockIdx.x * 8 + (slot)] = gtime(); \
+// `trace` is a kernel-local copy of g_gemm_trace, read once: a global read inside the
+// pipelined loops would be re-issued every k-block (the barrier asm clobbers memory).
+#define TRACE(slot)                                           \
+  do {                                                        \
+    if (trace) trace[blockIdx.x * 8 + (slot)] = gtime();     \
   } while (0)
 
 // One warp's 32 (MMA rows) x 32 (MMA cols) accumulator block -> Y.
@@ -195,7 +249,20 @@ __device__ __forceinline__ void epi_block_glu(const GemmArgs& g, __nv_bfloat16* 
   __syncwarp();
 }
 
-template <int kPair>
+// 32 accumulator columns at taddr, summed over the K-interleaved accumulators (fixed order).
+__device__ __forceinline__ void tmem_ld_sum(uint32_t taddr, int ka, uint32_t stride, uint32_t (&v)[32]) {
+  tmem_ld_32x32b_x32(taddr, v);
+  tmem_ld_wait();
+  for (int j = 1; j < ka; ++j) {
+    uint32_t w[32];
+    tmem_ld_32x32b_x32(taddr + (uint32_t)j * stride, w);
+    tmem_ld_wait();
+#pragma unroll
+    for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) + __uint_as_float(w[e]));
+  }
+}
+
+template <int kPair, int kMT>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
                              const __grid_constant__ CUtensorMap tmap_b, const GemmArgs g) {
@@ -203,27 +270,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int BN = g.BN;
   const int stages = g.stages;
+  constexpr int MT = kMT;
   const int bn_cta = BN / kPair;                       // B rows staged by this CTA
+  const uint32_t a_bytes = (uint32_t)MT * kABytes;     // A bytes per stage
   const uint32_t b_bytes = (uint32_t)bn_cta * kBK * 2;
   uint8_t* sA = smem;
-  uint8_t* sB = smem + (size_t)stages * kABytes;
+  uint8_t* sB = smem + (size_t)stages * a_bytes;
   __nv_bfloat16* stg_all = reinterpret_cast<__nv_bfloat16*>(sB + (size_t)stages * b_bytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stg_all) + 4 * kStgBytes);
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;  // 2
   uint64_t* tempty = tfull + 2;      // 2
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  int* flag_slot = reinterpret_cast<int*>(tmem_slot + 1);
 
+  unsigned long long* const trace = g_gemm_trace;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = (kPair == 2) ? cluster_ctarank() : 0u;
   const bool leader = rank == 0;
   const int cid = blockIdx.x / kPair;   // cluster (pair) id
   const int ncl = gridDim.x / kPair;
-  const uint32_t acc_stride = (uint32_t)BN;
+  const int KA = g.kacc;
+  const uint32_t sub_stride = (uint32_t)(MT * BN);          // one K-interleaved accumulator
+  const uint32_t acc_stride = (uint32_t)KA * sub_stride;    // TMEM columns per accumulator buffer
+  const int tile_rows = kBM * kPair * MT;           // MMA-space rows per tile
   uint32_t tmem_cols = 32;
-  while (tmem_cols < 2 * acc_stride) tmem_cols <<= 1;
+  while (tmem_cols < (uint32_t)g.nacc * acc_stride) tmem_cols <<= 1;
 
   if (threadIdx.x == 0) TRACE(0);
   if (warp == 0 && lane == 0) {
@@ -247,76 +319,108 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (kPair == 2) cluster_sync();  // peers' barriers/TMEM exist before any remote op
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
   if (threadIdx.x == 0) TRACE(1);
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ================= TMA producer (both CTAs) =================
-      const uint32_t full_leader0 = (kPair == 2) ? mapa_shared(&full[0], 0) : 0u;
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int u = cid; u < g.total_units; u += ncl) {
-        const int t = u / g.splits;
-        const int mt = t % g.m_tiles;
-        const int nt = t / g.m_tiles;
-        const int kb0 = (u % g.splits) * g.kb_per_split;
-        const int kb1 = min(g.num_kb, kb0 + g.kb_per_split);
-        const int arow = mt * (kBM * kPair) + (int)rank * kBM;
-        const int brow = nt * BN + (int)rank * bn_cta;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          if (kPair == 2) {
-            const uint32_t lbar = full_leader0 + (uint32_t)stage * 8u;
-            if (leader) mbar_arrive_expect_tx(&full[stage], kPair * (kABytes + b_bytes));
-            tma_load_2d_pair(sA + (size_t)stage * kABytes, &tmap_a, lbar, kb * kBK, arow, g.hint_a);
-            tma_load_2d_pair(sB + (size_t)stage * b_bytes, &tmap_b, lbar, kb * kBK, brow, g.hint_b);
-          } else {
-            mbar_arrive_expect_tx(&full[stage], kABytes + b_bytes);
-            tma_load_2d(sA + (size_t)stage * kABytes, &tmap_a, &full[stage], kb * kBK, arow, g.hint_a);
-            tma_load_2d(sB + (size_t)stage * b_bytes, &tmap_b, &full[stage], kb * kBK, brow, g.hint_b);
-          }
-          if (++stage == stages) { stage = 0; phase ^= 1; }
+    // ================= TMA producer (both CTAs; whole warp, one elected lane issues) =================
+    const uint32_t full_leader0 = (kPair == 2) ? mapa_shared(&full[0], 0) : 0u;
+    int stage = 0;
+    uint32_t phase = 0;
+    SegIter seg(g, cid, ncl);
+    int t, kb0, kb1;
+    while (seg.next(g, t, kb0, kb1)) {
+      const int mt = t % g.m_tiles;
+      const int nt = t / g.m_tiles;
+      const int arow = mt * tile_rows + (int)rank * kBM;
+      const int brow = nt * BN + (int)rank * bn_cta;
+      // blocked A: 128-row block r, k-block kb lives at rows (r * num_kb + kb) * 128, column 0
+      auto a_x = [&](int kb) { return g.a_blocked ? 0 : kb * kBK; };
+      auto a_y = [&](int kb, int i) {
+        const int r = arow + i * kBM * kPair;
+        return g.a_blocked ? ((r / kBM) * g.num_kb + kb) * kBM : r;
+      };
+      if (g.pf_dist > 0) {
+        for (int kb = kb0; kb < min(kb1, kb0 + g.pf_dist); ++kb)
+#pragma unroll
+          for (int i = 0; i < kMT; ++i) tma_prefetch_l2_2d_w(&tmap_a, a_x(kb), a_y(kb, i));
+      }
+      for (int kb = kb0; kb < kb1; ++kb) {
+        if (g.pf_dist > 0 && kb + g.pf_dist < kb1) {
+#pragma unroll
+          for (int i = 0; i < kMT; ++i) tma_prefetch_l2_2d_w(&tmap_a, a_x(kb + g.pf_dist), a_y(kb + g.pf_dist, i));
         }
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* a_dst = sA + (size_t)stage * a_bytes;
+        if (kPair == 1 && (g.dbg & 2)) {
+          mbar_arrive_w(&full[stage]);
+        } else if (kPair == 2) {
+          const uint32_t lbar = full_leader0 + (uint32_t)stage * 8u;
+          if (leader) mbar_arrive_expect_tx_w(&full[stage], kPair * (a_bytes + b_bytes));
+#pragma unroll
+          for (int i = 0; i < kMT; ++i)
+            tma_load_2d_pair_w(a_dst + (size_t)i * kABytes, &tmap_a, lbar, a_x(kb), a_y(kb, i), g.hint_a);
+          tma_load_2d_pair_w(sB + (size_t)stage * b_bytes, &tmap_b, lbar, kb * kBK, brow, g.hint_b);
+        } else {
+          mbar_arrive_expect_tx_w(&full[stage], a_bytes + b_bytes);
+#pragma unroll
+          for (int i = 0; i < kMT; ++i)
+            tma_load_2d_w(a_dst + (size_t)i * kABytes, &tmap_a, &full[stage], a_x(kb), a_y(kb, i), g.hint_a);
+          tma_load_2d_w(sB + (size_t)stage * b_bytes, &tmap_b, &full[stage], kb * kBK, brow, g.hint_b);
+        }
+        if (++stage == stages) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
-      // ================= MMA issuer (single thread of the leader CTA) =================
+    if (leader) {
+      // ================= MMA issuer (leader CTA; whole warp, one elected lane issues) =================
       const uint32_t idesc = make_idesc_bf16(kBM * kPair, BN);
+      const uint32_t ka_mask = (uint32_t)KA - 1u;
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = cid; u < g.total_units; u += ncl) {
-        const int kb0 = (u % g.splits) * g.kb_per_split;
-        const int kb1 = min(g.num_kb, kb0 + g.kb_per_split);
+      bool first = true;
+      SegIter seg(g, cid, ncl);
+      int t, kb0, kb1;
+      while (seg.next(g, t, kb0, kb1)) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)acc * acc_stride;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
-          if (u == cid && kb == kb0) TRACE(2);
-          if (u == cid && kb == kb1 - 1) TRACE(3);
+          if (lane == 0 && first && kb == kb0) TRACE(2);
+          if (lane == 0 && first && kb == kb1 - 1) TRACE(3);
           tc_fence_after();
-          const uint64_t adesc = make_sdesc_sw128(sA + (size_t)stage * kABytes);
-          const uint64_t bdesc = make_sdesc_sw128(sB + (size_t)stage * b_bytes);
+          if (kPair == 1 && (g.dbg & 1)) {
+            mbar_arrive_w(&empty[stage]);
+          } else {
+            const uint64_t bdesc = make_sdesc_sw128(sB + (size_t)stage * b_bytes);
+            const uint64_t adesc0 = make_sdesc_sw128(sA + (size_t)stage * a_bytes);
+            // kk outer, sub-tile inner: consecutive MMAs hit different accumulators
 #pragma unroll
-          for (int kk = 0; kk < kBK / 16; ++kk) {
-            // advance 16 elements (32 bytes) inside the swizzle atom: +2 in 16-byte units
-            const uint32_t accum = (kb > kb0 || kk > 0) ? 1u : 0u;
-            if (kPair == 2)
-              umma_bf16_pair(d_tmem, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2), idesc, accum);
-            else
-              umma_bf16(d_tmem, adesc + (uint64_t)(kk * 2), bdesc + (uint64_t)(kk * 2), idesc, accum);
+            for (int kk = 0; kk < kBK / 16; ++kk) {
+              // advance 16 elements (32 bytes) inside the swizzle atom: +2 in 16-byte units
+              const uint32_t j = (uint32_t)kk & ka_mask;
+              const uint32_t accum = (kb > kb0 || (uint32_t)kk > ka_mask) ? 1u : 0u;
+#pragma unroll
+              for (int i = 0; i < kMT; ++i) {
+                const uint64_t adesc = adesc0 + (uint64_t)((i * kABytes) >> 4) + (uint64_t)(kk * 2);
+                const uint32_t d = d_tmem + j * sub_stride + (uint32_t)(i * BN);
+                if (kPair == 2) umma_bf16_pair_w(d, adesc, bdesc + (uint64_t)(kk * 2), idesc, accum);
+                else umma_bf16_w(d, adesc, bdesc + (uint64_t)(kk * 2), idesc, accum);
+              }
+            }
+            if (kPair == 2) umma_commit_pair_mc_w(&empty[stage], 0x3);
+            else umma_commit_w(&empty[stage]);
           }
-          if (kPair == 2) umma_commit_pair_mc(&empty[stage], 0x3);
-          else umma_commit(&empty[stage]);
           if (++stage == stages) { stage = 0; phase ^= 1; }
         }
-        if (kPair == 2) umma_commit_pair_mc(&tfull[acc], 0x3);
-        else umma_commit(&tfull[acc]);
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        if (kPair == 2) umma_commit_pair_mc_w(&tfull[acc], 0x3);
+        else if (g.dbg & 1) mbar_arrive_w(&tfull[acc]);
+        else umma_commit_w(&tfull[acc]);
+        if (++acc == g.nacc) { acc = 0; acc_phase ^= 1; }
+        first = false;
       }
     }
   } else {
@@ -325,16 +429,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     __nv_bfloat16* stg = stg_all + (size_t)q * (kStgBytes / 2);
     const uint32_t tempty_leader0 = (kPair == 2) ? mapa_shared(&tempty[0], 0) : 0u;
     const int nchunk = BN / 32;
+    const size_t part_floats = (size_t)kBM * BN;  // one CTA's partial of one sub-tile
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = cid; u < g.total_units; u += ncl) {
-      const int t = u / g.splits;
-      const int sp = u % g.splits;
-      const int mt = t % g.m_tiles;
+    bool first = true;
+    SegIter seg(g, cid, ncl);
+    int t, kb0, kb1;
+    while (seg.next(g, t, kb0, kb1)) {
+      const int mtile = t % g.m_tiles;
       const int nt = t / g.m_tiles;
-      const int m0 = mt * (kBM * kPair) + (int)rank * kBM + q * 32;
+      const int mbase = mtile * tile_rows + (int)rank * kBM + q * 32;  // + i * kBM * kPair per sub-tile
       mbar_wait(&tfull[acc], acc_phase);
-      if (lane == 0 && q == 0 && u == cid) TRACE(4);
+      if (lane == 0 && q == 0 && first) TRACE(4);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)acc * acc_stride;
       auto release_acc = [&]() {
@@ -345,12 +451,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           else mbar_arrive(&tempty[acc]);
         }
       };
-      if (g.splits == 1) {
-        if (m0 < g.M_valid) {
+      if (kb0 == 0 && kb1 == g.num_kb) {
+        // whole tile in this segment: straight to Y
+        for (int i = 0; i < MT; ++i) {
+          const int m0 = mbase + i * kBM * kPair;
+          if (m0 >= g.M_valid) continue;
           for (int c = 0; c < BN; c += 32) {
             uint32_t v[32];
-            tmem_ld_32x32b_x32(tbase + c, v);
-            tmem_ld_wait();
+            tmem_ld_sum(tbase + (uint32_t)(i * BN + c), KA, sub_stride, v);
             if (nt * BN + c < g.N_valid) {
               if (g.glu) epi_block_glu(g, stg, lane, m0, nt * BN + c, v);
               else epi_block(g, stg, lane, m0, nt * BN + c, v);
@@ -359,55 +467,92 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         release_acc();
       } else {
-        // ---- deterministic split-K over this CTA's 128-row half of the tile
+        // ---- stream-K split tile (see SegIter): c_first..c_last-1 publish fp32 partials
+        // and signal; the finisher c_last adds them, in cluster order, to its own TMEM
+        // accumulator — no partial of its own, no reload.
+        const int x0 = t * g.num_kb;
+        const int c_first = sk_owner(g, x0, ncl);
+        const int c_last = sk_owner(g, x0 + g.num_kb - 1, ncl);
         const int region = t * kPair + (int)rank;
-        float* reg_ws = g.ws + (size_t)region * g.splits * kBM * BN;
-        float* mine = reg_ws + (size_t)sp * kBM * BN;
-        for (int c = 0; c < nchunk; ++c) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(tbase + c * 32, v);
-          tmem_ld_wait();
-          // lane-major layout: float4 j of lane l at (j*32 + l) -> 512 contiguous bytes per store
-          float4* dst = reinterpret_cast<float4*>(mine + ((size_t)c * 4 + q) * 1024) + lane;
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            dst[j * 32] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                                      __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
-        }
-        release_acc();
-        __threadfence();
-        named_bar_sync(1, 128);
-        if (q == 0 && lane == 0) {
-          const int prev = atomicAdd(&g.counters[region], 1);
-          const int last = (prev == g.splits - 1);
-          if (last) g.counters[region] = 0;  // re-arm for the next launch / graph replay
-          *flag_slot = last;
-        }
-        named_bar_sync(1, 128);
-        const bool last = *flag_slot != 0;
-        named_bar_sync(1, 128);  // flag consumed before the next unit may overwrite it
-        if (last) {
-          __threadfence();
-          if (m0 < g.M_valid) {
+        if (cid != c_last) {
+          float* mine = g.ws + (((size_t)cid * kPair + rank) * MT) * part_floats;
+          for (int i = 0; i < MT; ++i) {
             for (int c = 0; c < nchunk; ++c) {
+              uint32_t v[32];
+              tmem_ld_sum(tbase + (uint32_t)(i * BN + c * 32), KA, sub_stride, v);
+              // lane-major layout: float4 j of lane l at (j*32 + l) -> 512 contiguous bytes per store
+              float4* dst = reinterpret_cast<float4*>(mine + i * part_floats + ((size_t)c * 4 + q) * 1024) + lane;
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                __stcg(dst + j * 32, make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                                 __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3])));
+            }
+          }
+          release_acc();
+          __threadfence();
+          named_bar_sync(1, 128);
+          if (q == 0 && lane == 0) red_release_gpu_add(&g.counters[region], 1);
+        } else {
+          if (q == 0 && lane == 0) {
+            const int need = c_last - c_first;
+            while (ld_acquire_gpu(&g.counters[region]) < need) {
+            }
+            g.counters[region] = 0;  // re-arm for the next launch / graph replay
+          }
+          named_bar_sync(1, 128);
+          __threadfence();
+          for (int i = 0; i < MT; ++i) {
+            const int m0 = mbase + i * kBM * kPair;
+            for (int c = 0; c < nchunk; ++c) {
+              uint32_t v[32];
+              tmem_ld_sum(tbase + (uint32_t)(i * BN + c * 32), KA, sub_stride, v);
+              if (m0 >= g.M_valid) continue;
               float acc_v[32];
 #pragma unroll
-              for (int j = 0; j < 32; ++j) acc_v[j] = 0.f;
-              for (int s2 = 0; s2 < g.splits; ++s2) {
-                const float4* src = reinterpret_cast<const float4*>(
-                                        reg_ws + (size_t)s2 * kBM * BN + ((size_t)c * 4 + q) * 1024) + lane;
-                float4 f[8];
+              for (int j = 0; j < 32; ++j) acc_v[j] = __uint_as_float(v[j]);
+              int c2 = c_first;
+              for (; c2 + 1 < c_last; c2 += 2) {  // two contributors in flight
+                const float4* s0 = reinterpret_cast<const float4*>(
+                                       g.ws + (((size_t)c2 * kPair + rank) * MT + i) * part_floats +
+                                       ((size_t)c * 4 + q) * 1024) + lane;
+                const float4* s1 = reinterpret_cast<const float4*>(
+                                       g.ws + (((size_t)(c2 + 1) * kPair + rank) * MT + i) * part_floats +
+                                       ((size_t)c * 4 + q) * 1024) + lane;
+                float4 f0[8], f1[8];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) f[j] = __ldcg(src + j * 32);
+                for (int j = 0; j < 8; ++j) f0[j] = __ldcg(s0 + j * 32);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) f1[j] = __ldcg(s1 + j * 32);
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                  acc_v[4 * j] += f[j].x;
-                  acc_v[4 * j + 1] += f[j].y;
-                  acc_v[4 * j + 2] += f[j].z;
-                  acc_v[4 * j + 3] += f[j].w;
+                  acc_v[4 * j] += f0[j].x;
+                  acc_v[4 * j + 1] += f0[j].y;
+                  acc_v[4 * j + 2] += f0[j].z;
+                  acc_v[4 * j + 3] += f0[j].w;
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  acc_v[4 * j] += f1[j].x;
+                  acc_v[4 * j + 1] += f1[j].y;
+                  acc_v[4 * j + 2] += f1[j].z;
+                  acc_v[4 * j + 3] += f1[j].w;
                 }
               }
-              uint32_t v[32];
+              if (c2 < c_last) {
+                const float4* s0 = reinterpret_cast<const float4*>(
+                                       g.ws + (((size_t)c2 * kPair + rank) * MT + i) * part_floats +
+                                       ((size_t)c * 4 + q) * 1024) + lane;
+                float4 f0[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) f0[j] = __ldcg(s0 + j * 32);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  acc_v[4 * j] += f0[j].x;
+                  acc_v[4 * j + 1] += f0[j].y;
+                  acc_v[4 * j + 2] += f0[j].z;
+                  acc_v[4 * j + 3] += f0[j].w;
+                }
+              }
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(acc_v[j]);
               if (nt * BN + c * 32 < g.N_valid) {
@@ -416,10 +561,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           }
+          release_acc();
         }
       }
-      if (lane == 0 && q == 0 && u == cid) TRACE(5);
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (lane == 0 && q == 0 && first) TRACE(5);
+      if (++acc == g.nacc) { acc = 0; acc_phase ^= 1; }
+      first = false;
     }
   }
   tc_fence_before();
@@ -440,13 +587,20 @@ int gemm_set_trace(unsigned long long* buf) {
   return e == cudaSuccess ? 0 : set_cuda_error("gemm trace", e);
 }
 
-static int gemm_smem_bytes(int b_rows_per_cta, int stages) {
-  return stages * (kABytes + b_rows_per_cta * kBK * 2) + 4 * kStgBytes + 1024 /*align*/ + (2 * stages + 4) * 8 + 32;
+static int gemm_smem_bytes(int a_bytes, int b_rows_per_cta, int stages) {
+  return stages * (a_bytes + b_rows_per_cta * kBK * 2) + 4 * kStgBytes + 1024 /*align*/ + (2 * stages + 4) * 8 + 32;
 }
 
 static int g_force_pair = -1;  // debug override: -1 auto, 0 single-CTA, 1 CTA pair
 int gemm_set_pair_mode(int mode) {
   g_force_pair = mode;
+  return 0;
+}
+// debug override of the decode (swap-AB) schedule: -1 auto; else bit0 = 2 A sub-tiles
+// per tile, bit1 = stream-K (without it: data-parallel whole tiles)
+static int g_force_variant = -1;
+int gemm_set_variant(int v) {
+  g_force_variant = v;
   return 0;
 }
 
@@ -461,12 +615,15 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
   if (ldy % 8 || reinterpret_cast<uintptr_t>(Y) % 16 || (residual && reinterpret_cast<uintptr_t>(residual) % 16) ||
       (bias && reinterpret_cast<uintptr_t>(bias) % 16))
     return set_error("gemm: Y/residual/bias must be 16-byte aligned with ldy % 8 == 0");
-  const int glu = (mode & 4) ? 1 : 0;  // flag bit: fused SwiGLU epilogue
+  const int glu = (mode & 4) ? 1 : 0;      // flag bit: fused SwiGLU epilogue
+  const int blocked = (mode & 8) ? 1 : 0;  // flag bit: W is block-packed (see rb_pack_weight)
   mode &= 3;
   if (glu && (O % 32 != 0 || bias != nullptr || residual != nullptr))
     return set_error("gemm: SwiGLU epilogue needs O % 32 == 0 and no bias / residual");
   if (mode == 0) mode = (T <= 256) ? 2 : 1;
   const bool swap = (mode == 2);
+  if (blocked && (!swap || O % kBM != 0 || ldw != K))
+    return set_error("gemm: block-packed weights need swap-AB mode, O % 128 == 0 and a dense [O, K] buffer");
   if (num_sms <= 0) num_sms = 148;
   GemmArgs g{};
   const int M = swap ? O : T;  // MMA-space rows
@@ -478,48 +635,56 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
   } else {
     BN = 256;
   }
-  // CTA pair whenever the partition has >= 2 SMs and the tile is wide enough to split B
-  // CTA pairs halve the per-SM operand stream of the tensor-bound prefill tiles; decode
-  // (swap-AB) tiles measured faster single (short K-split units, latency-dominated).
-  int pair = (!swap && num_sms >= 2 && M > kBM) ? 2 : 1;
+  // CTA pairs halve the per-SM operand stream: prefill tiles always; decode (swap-AB)
+  // tiles when the batch tile is wide (each CTA of the pair stages BN/2 activation rows,
+  // halving the activation re-read that otherwise matches the weight bytes per k-block).
+  int pair = (num_sms >= 2 && M > kBM && (!swap || BN > 128 || (BN == 128 && num_sms < 100))) ? 2 : 1;
   if (g_force_pair == 0) pair = 1;
   if (g_force_pair == 1 && num_sms >= 2 && BN >= 32) pair = 2;
+  // Decode (swap-AB): stream-K balances the tiles x k-blocks over the partition (no wave
+  // quantization, small weight matrices spread over every SM). Two A sub-tiles per B stage
+  // (variant bit 0) measured slower once the MMA issue loop was lean: off by default.
+  int variant = swap ? 2 : 0;
+  if (swap && g_force_variant >= 0) variant = g_force_variant;
+  int MT = ((variant & 1) && 4 * BN <= 512 && M > kBM * pair) ? 2 : 1;
   const int bn_cta = BN / pair;
-  const int stage_bytes = kABytes + bn_cta * kBK * 2;
+  const int a_bytes = MT * kABytes;
+  const int stage_bytes = a_bytes + bn_cta * kBK * 2;
   int stages = (200 * 1024 - 4 * kStgBytes) / stage_bytes;
   if (stages > 8) stages = 8;
   if (stages < 2) stages = 2;
+  if (variant > 0 && ((variant >> 5) & 15) >= 2 && ((variant >> 5) & 15) <= stages) stages = (variant >> 5) & 15;
   g.BN = BN;
   g.stages = stages;
-  g.m_tiles = (M + kBM * pair - 1) / (kBM * pair);
+  g.mt = MT;
+  g.a_blocked = blocked;
+  g.pf_dist = (variant & 4) ? 8 : 0;
+  g.dbg = (pair == 1 && variant > 0) ? (variant >> 3) & 3 : 0;
+  int KA = 1;
+  if (variant > 0 && ((variant >> 9) & 3)) KA = 1 << ((variant >> 9) & 3);
+  while (KA > 1 && KA * MT * BN > 512) KA >>= 1;
+  g.kacc = KA;
+  g.nacc = (2 * KA * MT * BN <= 512) ? 2 : 1;
+  g.m_tiles = (M + kBM * pair * MT - 1) / (kBM * pair * MT);
   g.n_tiles = (N + BN - 1) / BN;
   g.num_kb = K / kBK;
   g.total_tiles = g.m_tiles * g.n_tiles;
-  const int slots = num_sms / pair;  // concurrent work-unit slots (clusters)
-  // split-K (decode / swap-AB only) when the tile count under-fills the partition.
-  // Each CTA is bound by its own L2->SMEM stream, so a work unit costs the bytes a CTA
-  // streams ((128 + BN/pair) x K/S x 2) plus, when split, writing its fp32 partial and
-  // the amortised fixed-order re-read (2 x 128 x BN x 4); minimise rounds x unit cost.
-  int splits = 1;
-  if (swap && workspace != nullptr && counters != nullptr && g.total_tiles * pair <= counters_len) {
-    const double stream_bytes = (double)(kBM + bn_cta) * K * 2.0;
-    const double part_bytes = 2.0 * kBM * BN * 4.0;
-    double best = (double)((g.total_tiles + slots - 1) / slots) * stream_bytes;
-    for (int s2 = 2; s2 <= 8; ++s2) {
-      if (g.num_kb / s2 < 4) break;
-      const size_t need = (size_t)g.total_tiles * pair * s2 * kBM * BN * sizeof(float);
-      if (need > ws_bytes) break;
-      const double rounds = (double)((g.total_tiles * s2 + slots - 1) / slots);
-      const double cost = rounds * (stream_bytes / s2 + part_bytes);
-      if (cost < 0.95 * best) {
-        best = cost;
-        splits = s2;
-      }
+  g.total_iters = g.total_tiles * g.num_kb;
+  const int slots = num_sms / pair;  // concurrent clusters
+  int clusters = g.total_tiles < slots ? g.total_tiles : slots;
+  g.streamk = 0;
+  if ((variant & 2) && workspace != nullptr && counters != nullptr && g.total_tiles * pair <= counters_len &&
+      g.total_tiles % slots != 0) {
+    // every cluster gets >= 8 k-blocks; one partial slot per cluster: [cluster][pair][MT][128 x BN] fp32
+    int ncl = slots;
+    if (g.total_iters / ncl < 8) ncl = g.total_iters / 8 > 0 ? g.total_iters / 8 : 1;
+    const size_t need = (size_t)ncl * pair * MT * kBM * BN * sizeof(float);
+    if (need <= ws_bytes && ncl > 0) {
+      g.streamk = 1;
+      clusters = ncl;
     }
   }
-  g.kb_per_split = (g.num_kb + splits - 1) / splits;
-  g.splits = (g.num_kb + g.kb_per_split - 1) / g.kb_per_split;
-  g.total_units = g.total_tiles * g.splits;
+  if (clusters < 1) clusters = 1;
   g.ws = reinterpret_cast<float*>(workspace);
   g.counters = counters;
   g.M_valid = M;
@@ -543,40 +708,36 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
   const void* b_ptr = swap ? X : W;
   const long long lda = swap ? ldw : ldx;
   const long long ldb = swap ? ldx : ldw;
-  int rc = make_tmap_2d_bf16(&ta, a_ptr, (uint64_t)K, (uint64_t)M, (uint64_t)lda, kBK, kBM);
+  int rc = blocked ? make_tmap_2d_bf16(&ta, a_ptr, (uint64_t)kBK, (uint64_t)M * (K / kBK), (uint64_t)kBK, kBK, kBM)
+                   : make_tmap_2d_bf16(&ta, a_ptr, (uint64_t)K, (uint64_t)M, (uint64_t)lda, kBK, kBM);
   if (rc) return rc;
   rc = make_tmap_2d_bf16(&tb, b_ptr, (uint64_t)K, (uint64_t)N, (uint64_t)ldb, kBK, bn_cta);
   if (rc) return rc;
 
-  const int smem = gemm_smem_bytes(bn_cta, stages);
-  static bool attr_done[2] = {false, false};
-  if (!attr_done[pair - 1]) {
-    cudaError_t e = cudaFuncSetAttribute(pair == 2 ? gemm_bf16_tcgen05_kernel<2> : gemm_bf16_tcgen05_kernel<1>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  const int smem = gemm_smem_bytes(a_bytes, bn_cta, stages);
+  using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const GemmArgs);
+  static const KernelFn kernels[2][2] = {{gemm_bf16_tcgen05_kernel<1, 1>, gemm_bf16_tcgen05_kernel<1, 2>},
+                                         {gemm_bf16_tcgen05_kernel<2, 1>, gemm_bf16_tcgen05_kernel<2, 2>}};
+  static bool attr_done[2][2] = {{false, false}, {false, false}};
+  const KernelFn kern = kernels[pair - 1][MT - 1];
+  if (!attr_done[pair - 1][MT - 1]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return set_cuda_error("gemm: set smem attr", e);
-    attr_done[pair - 1] = true;
+    attr_done[pair - 1][MT - 1] = true;
   }
-  int clusters = g.total_units < slots ? g.total_units : slots;
-  if (clusters < 1) clusters = 1;
-  cudaError_t e;
-  if (pair == 2) {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(2 * clusters);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, gemm_bf16_tcgen05_kernel<2>, ta, tb, g);
-  } else {
-    gemm_bf16_tcgen05_kernel<1><<<clusters, kThreads, smem, stream>>>(ta, tb, g);
-    e = cudaGetLastError();
-  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(pair * clusters);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = pair;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pair == 2 ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, g);
   if (e != cudaSuccess) return set_cuda_error("gemm launch", e);
   return 0;
 }

@@ -24,8 +24,12 @@ for (T, O, K, mode, sms) in shapes:
     flush.zero_()
     torch.cuda.synchronize()
     lib.rb_debug_gemm_trace(tr.data_ptr())
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
     ops.linear(x, w, out=y, mode=mode, num_sms=sms, scratch=sc)
+    ev1.record()
     torch.cuda.synchronize()
+    print(f"  event-timed launch: {ev0.elapsed_time(ev1) * 1e3:.2f} us")
     lib.rb_debug_gemm_trace(None)
     t = tr.view(148, 8).cpu()
     used = t[:, 0] > 0
