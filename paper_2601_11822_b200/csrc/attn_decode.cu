@@ -93,6 +93,8 @@ __device__ __forceinline__ void item_pages(const DecArgs& a, int item, int& b, i
 
 __global__ void __launch_bounds__(kWarps * 32, 1)
     decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map, const DecArgs a) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5;
@@ -296,6 +298,8 @@ __global__ void decode_attn_combine_kernel(const float* __restrict__ part_o, con
                                            const int* __restrict__ seq_lens, __nv_bfloat16* __restrict__ out,
                                            long long out_tok_stride, int Hkv, int G, int splits,
                                            int chunk_pages) {
+  pdl_trigger();
+  pdl_wait();
   const int b = blockIdx.x;
   const int hq = blockIdx.y;
   const int d = threadIdx.x;
@@ -384,13 +388,10 @@ int decode_attention_launch(const void* q, long long q_tok_stride, const void* c
   int grid = (int)((warps_needed + kWarps - 1) / kWarps);
   if (grid > num_sms) grid = num_sms;
   if (grid < 1) grid = 1;
-  decode_attn_tc_kernel<<<grid, kWarps * 32, smem, st>>>(map, a);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_k(decode_attn_tc_kernel, dim3(grid), dim3(kWarps * 32), smem, st, 1, map, a);
   if (e != cudaSuccess) return set_cuda_error("decode attn launch", e);
   if (splits > 1) {
-    decode_attn_combine_kernel<<<dim3(B, Hq), kD, 0, st>>>(a.part_o, a.part_ml, seq_lens, a.out, out_tok_stride,
-                                                           Hkv, G, splits, chunk_pages);
-    e = cudaGetLastError();
+    e = launch_k(decode_attn_combine_kernel, dim3(B, Hq), dim3(kD), 0, st, 1, a.part_o, a.part_ml, seq_lens, a.out, out_tok_stride, Hkv, G, splits, chunk_pages);
     if (e != cudaSuccess) return set_cuda_error("decode combine launch", e);
   }
   return 0;

@@ -62,6 +62,8 @@ __global__ void __launch_bounds__(kPMaxWarps * 32)
                         const __nv_bfloat16* __restrict__ cache, const int* __restrict__ bt, int T, int start,
                         int Hq, int Hkv, int PB, __nv_bfloat16* __restrict__ out, long long out_tok_stride,
                         float scale_log2) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(128) uint8_t smem[];
   const int G = Hq / Hkv;
   const int nwarps = G * PB;
@@ -262,11 +264,7 @@ int prefill_attention_launch(const void* q, long long q_tok_stride, const void* 
     attr = true;
   }
   dim3 grid((T + 16 * PB - 1) / (16 * PB), Hkv);
-  prefill_attn_kernel<<<grid, nwarps * 32, smem, st>>>((const __nv_bfloat16*)q, q_tok_stride,
-                                                       (const __nv_bfloat16*)cache_layer, bt, T, start, Hq, Hkv, PB,
-                                                       (__nv_bfloat16*)out, out_tok_stride,
-                                                       scale * 1.4426950408889634f);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_k(prefill_attn_kernel, dim3(grid), dim3(nwarps * 32), smem, st, 1, (const __nv_bfloat16*)q, q_tok_stride, (const __nv_bfloat16*)cache_layer, bt, T, start, Hq, Hkv, PB, (__nv_bfloat16*)out, out_tok_stride, scale * 1.4426950408889634f);
   if (e != cudaSuccess) return set_cuda_error("prefill attn launch", e);
   return 0;
 }

@@ -85,6 +85,8 @@ __global__ void __launch_bounds__(fa::kThreads, 1)
     prefill_attn_tc_kernel(const __grid_constant__ CUtensorMap q_map, const __grid_constant__ CUtensorMap kv_map,
                            const int* __restrict__ bt, int T, int start, int Hq, int Hkv,
                            __nv_bfloat16* __restrict__ out, long long out_tok_stride, float scale_log2) {
+  pdl_trigger();
+  pdl_wait();
   using namespace fa;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -366,10 +368,7 @@ int prefill_attention_tc_launch(const void* q, long long q_tok_stride, const voi
     attr = true;
   }
   dim3 grid((T + kBMq - 1) / kBMq, Hq);
-  prefill_attn_tc_kernel<<<grid, kThreads, smem, st>>>(qmap, kvmap, bt, T, start, Hq, Hkv,
-                                                       reinterpret_cast<__nv_bfloat16*>(out), out_tok_stride,
-                                                       scale * 1.4426950408889634f);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_k(prefill_attn_tc_kernel, dim3(grid), dim3(kThreads), smem, st, 1, qmap, kvmap, bt, T, start, Hq, Hkv, reinterpret_cast<__nv_bfloat16*>(out), out_tok_stride, scale * 1.4426950408889634f);
   if (e != cudaSuccess) return set_cuda_error("prefill attn tc launch", e);
   return 0;
 }

@@ -42,6 +42,10 @@ const char* rb_last_error(void) { return rb::last_error(); }
 int rb_debug_gemm_trace(unsigned long long* buf) { return rb::gemm_set_trace(buf); }
 int rb_debug_gemm_pair_mode(int mode) { return rb::gemm_set_pair_mode(mode); }
 int rb_debug_gemm_variant(int v) { return rb::gemm_set_variant(v); }
+int rb_set_pdl(int on) {
+  rb::set_pdl(on != 0);
+  return 0;
+}
 
 int rb_device_sm_count(int device, int* out) {
   cudaError_t e = cudaDeviceGetAttribute(out, cudaDevAttrMultiProcessorCount, device);

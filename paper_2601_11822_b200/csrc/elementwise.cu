@@ -15,6 +15,8 @@ namespace rb {
 // y = x * rsqrt(mean(x^2) + eps) * w   (fp32 math, bf16 io), one CTA per row.
 __global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, long long ldx, const __nv_bfloat16* __restrict__ w,
                                __nv_bfloat16* __restrict__ y, long long ldy, int H, float eps) {
+  pdl_trigger();
+  pdl_wait();
   const int row = blockIdx.x;
   const __nv_bfloat16* xr = x + (size_t)row * ldx;
   __nv_bfloat16* yr = y + (size_t)row * ldy;
@@ -64,9 +66,7 @@ int rmsnorm_launch(const void* x, long long ldx, const void* w, void* y, long lo
   int threads = H / 8;
   if (threads > 1024) threads = 1024;
   threads = ((threads + 31) / 32) * 32;
-  rmsnorm_kernel<<<T, threads, 0, st>>>((const __nv_bfloat16*)x, ldx, (const __nv_bfloat16*)w, (__nv_bfloat16*)y,
-                                        ldy, H, eps);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_k(rmsnorm_kernel, dim3(T), dim3(threads), 0, st, 1, (const __nv_bfloat16*)x, ldx, (const __nv_bfloat16*)w, (__nv_bfloat16*)y, ldy, H, eps);
   return e == cudaSuccess ? 0 : set_cuda_error("rmsnorm launch", e);
 }
 
@@ -80,6 +80,8 @@ __global__ void rope_cache_kernel(const __nv_bfloat16* __restrict__ qkv, long lo
                                   const int* __restrict__ block_table, int bt_stride,
                                   const float* __restrict__ cos_sin, __nv_bfloat16* __restrict__ q_out,
                                   long long ld_q, __nv_bfloat16* __restrict__ cache, int Hq, int Hkv, int D) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x;
   const int p = pos[t];
   if (p < 0) return;
@@ -128,15 +130,15 @@ int rope_cache_launch(const void* qkv, long long ld_qkv, const int* pos, const i
                       int Hq, int Hkv, int D, cudaStream_t st) {
   if (T <= 0) return 0;
   if (D % 8) return set_error("rope: head dim must be a multiple of 8");
-  rope_cache_kernel<<<T, 256, 0, st>>>((const __nv_bfloat16*)qkv, ld_qkv, pos, tok_slot, bt, bt_stride, cos_sin,
-                                       (__nv_bfloat16*)q_out, ld_q, (__nv_bfloat16*)cache_layer, Hq, Hkv, D);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_k(rope_cache_kernel, dim3(T), dim3(256), 0, st, 1, (const __nv_bfloat16*)qkv, ld_qkv, pos, tok_slot, bt, bt_stride, cos_sin, (__nv_bfloat16*)q_out, ld_q, (__nv_bfloat16*)cache_layer, Hq, Hkv, D);
   return e == cudaSuccess ? 0 : set_cuda_error("rope launch", e);
 }
 
 // ------------------------------------------------------------------ SiLU(gate) * up
 __global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, long long ld_gu, __nv_bfloat16* __restrict__ y,
                                 long long ldy, int I) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.y;
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (i >= I) return;
@@ -161,8 +163,7 @@ int silu_mul_launch(const void* gu, long long ld_gu, void* y, long long ldy, int
   if (T <= 0) return 0;
   if (I % 8) return set_error("silu_mul: I must be a multiple of 8");
   dim3 grid((I / 8 + 255) / 256, T);
-  silu_mul_kernel<<<grid, 256, 0, st>>>((const __nv_bfloat16*)gu, ld_gu, (__nv_bfloat16*)y, ldy, I);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_k(silu_mul_kernel, dim3(grid), dim3(256), 0, st, 1, (const __nv_bfloat16*)gu, ld_gu, (__nv_bfloat16*)y, ldy, I);
   return e == cudaSuccess ? 0 : set_cuda_error("silu_mul launch", e);
 }
 
@@ -170,6 +171,8 @@ int silu_mul_launch(const void* gu, long long ld_gu, void* y, long long ldy, int
 // fused-SwiGLU GEMM epilogue expects); used where the GEMM runs unfused (decode).
 __global__ void silu_mul_il_kernel(const __nv_bfloat16* __restrict__ gu, long long ld_gu,
                                    __nv_bfloat16* __restrict__ y, long long ldy, int I) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.y;
   const int f = (blockIdx.x * blockDim.x + threadIdx.x) * 8;  // 8 features, inside one 16-block
   if (f >= I) return;
@@ -193,8 +196,7 @@ int silu_mul_interleaved_launch(const void* gu, long long ld_gu, void* y, long l
   if (T <= 0) return 0;
   if (I % 16) return set_error("silu_mul_interleaved: I must be a multiple of 16");
   dim3 grid((I / 8 + 255) / 256, T);
-  silu_mul_il_kernel<<<grid, 256, 0, st>>>((const __nv_bfloat16*)gu, ld_gu, (__nv_bfloat16*)y, ldy, I);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_k(silu_mul_il_kernel, dim3(grid), dim3(256), 0, st, 1, (const __nv_bfloat16*)gu, ld_gu, (__nv_bfloat16*)y, ldy, I);
   return e == cudaSuccess ? 0 : set_cuda_error("silu_mul_interleaved launch", e);
 }
 
@@ -205,6 +207,8 @@ int silu_mul_interleaved_launch(const void* gu, long long ld_gu, void* y, long l
 __global__ void embed_kernel(const int* __restrict__ ids, const int* __restrict__ slot_of_row,
                              const int* __restrict__ last_tok, const __nv_bfloat16* __restrict__ table,
                              __nv_bfloat16* __restrict__ y, int H, int* __restrict__ ids_out) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x;
   const int id = slot_of_row ? last_tok[slot_of_row[t]] : ids[t];
   if (threadIdx.x == 0 && ids_out) ids_out[t] = id;
@@ -216,9 +220,7 @@ __global__ void embed_kernel(const int* __restrict__ ids, const int* __restrict_
 int embed_launch(const int* ids, const int* slot_of_row, const int* last_tok, const void* table, void* y, int T, int H,
                  int* ids_out, cudaStream_t st) {
   if (T <= 0) return 0;
-  embed_kernel<<<T, 128, 0, st>>>(ids, slot_of_row, last_tok, (const __nv_bfloat16*)table, (__nv_bfloat16*)y, H,
-                                  ids_out);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_k(embed_kernel, dim3(T), dim3(128), 0, st, 1, ids, slot_of_row, last_tok, (const __nv_bfloat16*)table, (__nv_bfloat16*)y, H, ids_out);
   return e == cudaSuccess ? 0 : set_cuda_error("embed launch", e);
 }
 
@@ -228,6 +230,8 @@ int embed_launch(const int* ids, const int* slot_of_row, const int* last_tok, co
 __global__ void argmax_kernel(const __nv_bfloat16* __restrict__ logits, long long ld, int V, int* __restrict__ out,
                               const int* __restrict__ slot_of_row, int* __restrict__ last_tok,
                               const int* __restrict__ row_valid) {
+  pdl_trigger();
+  pdl_wait();
   const int row = blockIdx.x;
   if (row_valid && row_valid[row] <= 0) return;
   const __nv_bfloat16* x = logits + (size_t)row * ld;
@@ -281,8 +285,7 @@ int argmax_launch(const void* logits, long long ld, int T, int V, int* out, cons
                   const int* row_valid, cudaStream_t st) {
   if (T <= 0) return 0;
   if (V % 8 || ld % 8) return set_error("argmax: V and ld must be multiples of 8");
-  argmax_kernel<<<T, 512, 0, st>>>((const __nv_bfloat16*)logits, ld, V, out, slot_of_row, last_tok, row_valid);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_k(argmax_kernel, dim3(T), dim3(512), 0, st, 1, (const __nv_bfloat16*)logits, ld, V, out, slot_of_row, last_tok, row_valid);
   return e == cudaSuccess ? 0 : set_cuda_error("argmax launch", e);
 }
 
@@ -290,6 +293,8 @@ int argmax_launch(const void* logits, long long ld, int T, int V, int* out, cons
 // upd = [count, (slot, index, block) x count]; applied on device so a decode
 // graph replay only needs a small H2D copy of the step's new pages.
 __global__ void bt_update_kernel(const int* __restrict__ upd, int* __restrict__ block_table, int bt_stride) {
+  pdl_trigger();
+  pdl_wait();
   const int n = upd[0];
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int slot = upd[1 + 3 * i];
@@ -303,19 +308,19 @@ int bt_update_launch(const int* upd, int* block_table, int bt_stride, int max_up
   int threads = 256;
   int blocks = (max_updates + threads - 1) / threads;
   if (blocks < 1) blocks = 1;
-  bt_update_kernel<<<blocks, threads, 0, st>>>(upd, block_table, bt_stride);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_k(bt_update_kernel, dim3(blocks), dim3(threads), 0, st, 1, upd, block_table, bt_stride);
   return e == cudaSuccess ? 0 : set_cuda_error("bt_update launch", e);
 }
 
 // set last_tok[slot] = value (prefill completion hands the next input token to decode)
 __global__ void set_last_tok_kernel(int* last_tok, int slot, const int* value_ptr, int value) {
+  pdl_trigger();
+  pdl_wait();
   last_tok[slot] = value_ptr ? *value_ptr : value;
 }
 
 int set_last_tok_launch(int* last_tok, int slot, const int* value_ptr, int value, cudaStream_t st) {
-  set_last_tok_kernel<<<1, 1, 0, st>>>(last_tok, slot, value_ptr, value);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_k(set_last_tok_kernel, dim3(1), dim3(1), 0, st, 1, last_tok, slot, value_ptr, value);
   return e == cudaSuccess ? 0 : set_cuda_error("set_last_tok launch", e);
 }
 

@@ -321,6 +321,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
   if (threadIdx.x == 0) TRACE(1);
+  pdl_trigger();  // the next kernel may start its prologue as our CTAs drain
+  if (warp == 0) {
+    // Weights do not depend on the preceding kernel: warm L2 with this CTA's first
+    // k-blocks of them while that kernel finishes, then wait for its outputs.
+    SegIter s0(g, cid, ncl);
+    int t, kb0, kb1;
+    if (s0.next(g, t, kb0, kb1)) {
+      const int mt = t % g.m_tiles;
+      const int nt = t / g.m_tiles;
+      const int kend = min(kb1, kb0 + stages);
+      for (int kb = kb0; kb < kend; ++kb) {
+        if (g.swap) {
+          const int r0 = mt * tile_rows + (int)rank * kBM;
+#pragma unroll
+          for (int i = 0; i < kMT; ++i) {
+            const int r = r0 + i * kBM * kPair;
+            if (g.a_blocked) tma_prefetch_l2_2d_w(&tmap_a, 0, ((r / kBM) * g.num_kb + kb) * kBM);
+            else tma_prefetch_l2_2d_w(&tmap_a, kb * kBK, r);
+          }
+        } else {
+          tma_prefetch_l2_2d_w(&tmap_b, kb * kBK, nt * BN + (int)rank * bn_cta);
+        }
+      }
+    }
+  }
+  pdl_wait();
 
   if (warp == 0) {
     // ================= TMA producer (both CTAs; whole warp, one elected lane issues) =================
@@ -645,7 +671,7 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
   // quantization, small weight matrices spread over every SM). Two A sub-tiles per B stage
   // (variant bit 0) measured slower once the MMA issue loop was lean: off by default.
   int variant = swap ? 2 : 0;
-  if (swap && g_force_variant >= 0) variant = g_force_variant;
+  if (g_force_variant >= 0) variant = swap ? g_force_variant : (g_force_variant & ~1);
   int MT = ((variant & 1) && 4 * BN <= 512 && M > kBM * pair) ? 2 : 1;
   const int bn_cta = BN / pair;
   const int a_bytes = MT * kABytes;
@@ -725,19 +751,7 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
     if (e != cudaSuccess) return set_cuda_error("gemm: set smem attr", e);
     attr_done[pair - 1][MT - 1] = true;
   }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(pair * clusters);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = pair;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pair == 2 ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, g);
+  cudaError_t e = launch_k(kern, dim3(pair * clusters), dim3(kThreads), smem, stream, pair, ta, tb, g);
   if (e != cudaSuccess) return set_cuda_error("gemm launch", e);
   return 0;
 }

@@ -311,6 +311,13 @@ __device__ __forceinline__ void tma_prefetch_l2_2d_w(const void* tmap, int32_t x
       : "memory");
 }
 
+// ---------------------------------------------------------------- PDL
+// Let the next kernel in the stream launch (its CTAs park in pdl_wait until we finish).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// Block until the preceding kernel has completed and its writes are visible (no-op
+// when this kernel was not launched with programmatic stream serialization).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---------------------------------------------------------------- gpu-scope flags
 __device__ __forceinline__ void red_release_gpu_add(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");

@@ -23,6 +23,40 @@ void* driver_symbol(const char* name);
 int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
                       uint32_t box_inner, uint32_t box_outer);
 
+// Programmatic dependent launch (PDL): kernels of the forward are launched with
+// programmaticStreamSerialization so kernel N+1's CTAs start (prologue, weight
+// prefetch) while kernel N drains; every such kernel calls griddepcontrol.wait before
+// touching its predecessors' outputs (pdl_wait in ptx.cuh). rb_set_pdl(0) disables it.
+bool pdl_enabled();
+void set_pdl(bool on);
+
+template <typename... Exp, typename... Act>
+cudaError_t launch_k(void (*kernel)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int cluster,
+                     Act&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  unsigned n = 0;
+  if (cluster > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = cluster;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<Act&&>(args)...);
+}
+
 int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, const void* residual, int T,
                      int O, int K, long long ldx, long long ldw, long long ldy, int mode, int num_sms,
                      void* workspace, size_t ws_bytes, int* counters, int counters_len, cudaStream_t stream);

@@ -55,6 +55,7 @@ def main():
     ap.add_argument("--sms", type=int, default=72)
     ap.add_argument("--batches", default="16,64,128,256")
     ap.add_argument("--variants", default="auto")
+    ap.add_argument("--mode", type=int, default=2, help="2 = decode swap-AB (batches = B); 1 = prefill (batches = T)")
     args = ap.parse_args()
     dev = torch.device("cuda", torch.cuda.current_device())
     lib = ops.load()
@@ -87,7 +88,7 @@ def main():
                     if tk.startswith("ka"):
                         v |= {1: 0, 2: 1, 4: 2, 8: 3}[int(tk[2:])] << 9
                 lib.rb_debug_gemm_variant(-1 if "auto" in toks else v)
-                mode = 2 | (8 if "blk" in toks else 0)
+                mode = args.mode | (8 if "blk" in toks else 0)
                 wv = wp if "blk" in toks else w
                 y.fill_(float("nan"))
                 torch.cuda.synchronize()
@@ -99,6 +100,7 @@ def main():
                                 stream, flush)
                 row[f"{var}_us"] = round(ms * 1e3, 2)
                 row[f"{var}_tbs"] = round(O * K * 2 / ms / 1e9, 2)
+                row[f"{var}_tflops"] = round(2 * B * O * K / ms / 1e9)
                 if err > 1e-2:
                     row[f"{var}_err"] = float(f"{err:.2e}")
                 tot[(B, var)] = tot.get((B, var), 0.0) + ms * 1e3
@@ -106,6 +108,7 @@ def main():
             lib.rb_debug_gemm_variant(-1)
             ms = graph_time(lambda: torch.matmul(x, w.T, out=y), stream, flush)
             row["cublas_us"] = round(ms * 1e3, 2)
+            row["cublas_tflops"] = round(2 * B * O * K / ms / 1e9)
             row["cublas_tbs"] = round(O * K * 2 / ms / 1e9, 2)
             tot[(B, "cublas")] = tot.get((B, "cublas"), 0.0) + ms * 1e3
             print(json.dumps(row), flush=True)
