@@ -94,6 +94,20 @@ int rb_rope_cache_write(const void* qkv, long long ld_qkv, const int* pos, const
                         const int* block_table, int bt_stride, const float* cos_sin, void* q_out, long long ld_q,
                         void* cache_layer, int T, int Hq, int Hkv, int head_dim, void* stream);
 
+/* K1 + K5 fused — QKV projection whose epilogue applies RoPE and writes the paged KV:
+ *   qkv = X W^T (+bias); q heads rotated -> q_out[t]; k heads rotated and v heads
+ *   -> cache_layer[block_table[tok_slot[t]][pos[t]/16]][K|V][h][pos[t]%16]; pos[t] < 0 skips.
+ * W: [(Hq+2Hkv)*128, K] with the q and k rows of every head pair-interleaved (row 2j holds
+ * rotate-half dim j, row 2j+1 dim j+64; v rows unchanged), so attention scores are
+ * unchanged and each RoPE pair is adjacent in the accumulator.
+ * Replaces, in one launch, the compute term of prefill_time (costmodel.py:104) / weight
+ * term of decode_time (:130) for the QKV projection and the KV-write terms (:105, :132).
+ * mode / num_sms / workspace / counters as rb_gemm_bf16; head_dim must be 128. */
+int rb_gemm_qkv_rope(const void* X, const void* W, const void* bias, int T, int K, long long ldx, int Hq, int Hkv,
+                     int head_dim, const int* pos, const int* tok_slot, const int* block_table, int bt_stride,
+                     const float* cos_sin, void* q_out, long long ld_q, void* cache_layer, int mode, int num_sms,
+                     void* workspace, size_t ws_bytes, int* counters, int counters_len, void* stream);
+
 /* K5 — small fused ops (part of fixed_iteration_overhead_us, costmodel.py:53). */
 int rb_rmsnorm(const void* x, long long ldx, const void* w, void* y, long long ldy, int T, int H, float eps,
                void* stream);
@@ -136,6 +150,10 @@ typedef struct {
   int bt_stride;
   const float* cos_sin;
   int* last_tok;
+  /* 0: q/k weight rows in the standard rotate-half order (separate RoPE + cache-write
+   * kernel); 1: q/k rows pair-interleaved within each head (row 2j = dim j, 2j+1 = dim
+   * j+64), RoPE and the paged K/V write fused into the QKV GEMM epilogue. */
+  int qk_layout;
 } rb_model_t;
 
 typedef struct {

@@ -59,6 +59,16 @@ int rb_gemm_bf16(const void* X, const void* W, void* Y, const void* bias, const 
                               counters_len, ST(stream));
 }
 
+int rb_gemm_qkv_rope(const void* X, const void* W, const void* bias, int T, int K, long long ldx, int Hq, int Hkv,
+                     int head_dim, const int* pos, const int* tok_slot, const int* block_table, int bt_stride,
+                     const float* cos_sin, void* q_out, long long ld_q, void* cache_layer, int mode, int num_sms,
+                     void* workspace, size_t ws_bytes, int* counters, int counters_len, void* stream) {
+  const int nq = (Hq + 2 * Hkv) * head_dim;
+  const rb::GemmRope rp{pos, tok_slot, block_table, bt_stride, cos_sin, q_out, ld_q, cache_layer, Hq, Hkv, head_dim};
+  return rb::gemm_bf16_launch(X, W, q_out, bias, nullptr, T, nq, K, ldx, K, ld_q, mode, num_sms, workspace, ws_bytes,
+                              counters, counters_len, ST(stream), &rp);
+}
+
 int rb_decode_attention(const void* q, long long q_tok_stride, const void* cache_layer, const int* block_table,
                         int bt_stride, const int* row_slot, const int* seq_lens, void* out,
                         long long out_tok_stride, void* workspace, size_t ws_bytes, int B, int Hq, int Hkv,

@@ -72,10 +72,19 @@ extern "C" int rb_decoder_forward(const rb_model_t* m, const rb_workspace_t* w, 
   for (int l = 0; l < m->layers; ++l) {
     char* cache = static_cast<char*>(m->kv_cache) + (size_t)l * m->kv_layer_stride_bytes;
     RB_TRY(rmsnorm_launch(x, H, m->ln1[l], h, H, T, H, m->rms_eps, st));
-    RB_TRY(gemm_bf16_launch(h, m->wqkv[l], qkv, m->bqkv ? m->bqkv[l] : nullptr, nullptr, T, nq, H, H, H, nq, 0, sms,
-                            w->gemm_ws, w->gemm_ws_bytes, w->gemm_counters, w->gemm_counters_len, st));
-    RB_TRY(rope_cache_launch(qkv, nq, w->pos, w->slot, m->block_table, m->bt_stride, m->cos_sin, q, Hq * D, cache, T,
-                             Hq, Hkv, D, st));
+    if (m->qk_layout == 1) {
+      // q|k rows pair-interleaved: RoPE and the paged K/V write run in the QKV GEMM's
+      // epilogue (no qkv round trip through HBM, no separate RoPE kernel)
+      const GemmRope rp{w->pos, w->slot, m->block_table, m->bt_stride, m->cos_sin, q, (long long)Hq * D, cache,
+                        Hq, Hkv, D};
+      RB_TRY(gemm_bf16_launch(h, m->wqkv[l], qkv, m->bqkv ? m->bqkv[l] : nullptr, nullptr, T, nq, H, H, H, nq, 0,
+                              sms, w->gemm_ws, w->gemm_ws_bytes, w->gemm_counters, w->gemm_counters_len, st, &rp));
+    } else {
+      RB_TRY(gemm_bf16_launch(h, m->wqkv[l], qkv, m->bqkv ? m->bqkv[l] : nullptr, nullptr, T, nq, H, H, H, nq, 0,
+                              sms, w->gemm_ws, w->gemm_ws_bytes, w->gemm_counters, w->gemm_counters_len, st));
+      RB_TRY(rope_cache_launch(qkv, nq, w->pos, w->slot, m->block_table, m->bt_stride, m->cos_sin, q, Hq * D, cache,
+                               T, Hq, Hkv, D, st));
+    }
     if (nd > 0)
       RB_TRY(decode_attention_launch(q, (long long)Hq * D, cache, m->block_table, m->bt_stride, w->slot, w->seq, attn,
                                      (long long)Hq * D, w->attn_ws, w->attn_ws_bytes, nd, Hq, Hkv, D, b->max_pages,

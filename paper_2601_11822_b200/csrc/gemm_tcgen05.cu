@@ -63,6 +63,7 @@ struct GemmArgs {
   uint64_t hint_a, hint_b;
   float* ws;      // stream-K partials [cluster][rank][mt][BN/32][4 warps][8][32 lanes] float4
   int* counters;  // per (tile, rank), self-resetting
+  GemmRope rp;    // rp.q_out != nullptr: fused RoPE + paged K/V write epilogue (QKV projection)
 };
 
 // Work schedule shared by the producer, MMA and epilogue roles. Data-parallel: whole
@@ -123,6 +124,85 @@ __device__ __forceinline__ unsigned long long gtime() {
     if (trace) trace[blockIdx.x * 8 + (slot)] = gtime();     \
   } while (0)
 
+// Fused QKV epilogue readback: this lane's 8 columns [col, col+8) of 4 token rows.
+// q|k heads arrive with their RoPE pairs adjacent (pair-interleaved weight rows, see
+// model.interleave_rope_pairs: column 2j <-> rotate-half dim j, 2j+1 <-> dim j+64), so
+// the rotation is local to the 8 values; q goes to q_out, k/v straight into the token's
+// paged cache slot [page][K|V][kv-head][pos & 15][128]. Rows with pos < 0 (padding) skip.
+__device__ __forceinline__ void rope_readback(const GemmArgs& g, const __nv_bfloat16* stg, int lane, int row0,
+                                              int col, int rows_valid) {
+  const GemmRope& r = g.rp;
+  const int head = col >> 7;  // uniform over the 4 rows this lane handles
+  const int d = col & 127;
+  const bool rot = head < r.hq + r.hkv;
+  const bool is_q = head < r.hq;
+  const int is_v = head >= r.hq + r.hkv ? 1 : 0;
+  const int hk = head - r.hq - is_v * r.hkv;
+  // dependent loads batched over the 4 rows: pos/slot -> cos,sin / block-table page
+  int p[4], sl[4], page[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = row0 + i * 8 + (lane >> 2);
+    p[i] = row < rows_valid ? __ldg(r.pos + row) : -1;
+    sl[i] = is_q ? 0 : __ldg(r.tok_slot + min(row, rows_valid - 1));
+  }
+  float4 c[4], sn[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int pp = max(p[i], 0);
+    if (rot) {
+      const float* t = r.cos_sin + (size_t)pp * 128 + (d >> 1);
+      c[i] = __ldg(reinterpret_cast<const float4*>(t));
+      sn[i] = __ldg(reinterpret_cast<const float4*>(t + 64));
+    }
+    page[i] = is_q ? 0 : __ldg(r.block_table + (size_t)sl[i] * r.bt_stride + (pp >> 4));
+  }
+  float bv[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) bv[j] = 0.f;
+  if (g.bias) {
+    const uint4 b = *reinterpret_cast<const uint4*>(g.bias + col);
+    const uint32_t w[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float2 f = unpack_bf16x2(w[j]);
+      bv[2 * j] = f.x;
+      bv[2 * j + 1] = f.y;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (p[i] < 0) continue;
+    const int rl = i * 8 + (lane >> 2);
+    const uint4 sv = *reinterpret_cast<const uint4*>(stg + rl * kStgStride + (lane & 3) * 8);
+    const uint32_t w[4] = {sv.x, sv.y, sv.z, sv.w};
+    float x[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float2 f = unpack_bf16x2(w[j]);
+      x[2 * j] = f.x + bv[2 * j];
+      x[2 * j + 1] = f.y + bv[2 * j + 1];
+    }
+    if (rot) {
+      const float cc[4] = {c[i].x, c[i].y, c[i].z, c[i].w};
+      const float ss[4] = {sn[i].x, sn[i].y, sn[i].z, sn[i].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float x0 = x[2 * j], x1 = x[2 * j + 1];
+        x[2 * j] = x0 * cc[j] - x1 * ss[j];
+        x[2 * j + 1] = x1 * cc[j] + x0 * ss[j];
+      }
+    }
+    const int row = row0 + rl;
+    __nv_bfloat16* dst =
+        is_q ? static_cast<__nv_bfloat16*>(r.q_out) + (long long)row * r.ld_q + col
+             : static_cast<__nv_bfloat16*>(r.cache) + (((size_t)page[i] * 2 + is_v) * r.hkv + hk) * (16 * 128) +
+                   (size_t)(p[i] & 15) * 128 + d;
+    *reinterpret_cast<uint4*>(dst) = make_uint4(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3]),
+                                                pack_bf16x2(x[4], x[5]), pack_bf16x2(x[6], x[7]));
+  }
+}
+
 // One warp's 32 (MMA rows) x 32 (MMA cols) accumulator block -> Y.
 __device__ __forceinline__ void epi_block(const GemmArgs& g, __nv_bfloat16* stg, int lane, int m0, int n0,
                                           const uint32_t (&v)[32]) {
@@ -145,6 +225,11 @@ __device__ __forceinline__ void epi_block(const GemmArgs& g, __nv_bfloat16* stg,
   const int rows_valid = g.swap ? g.N_valid : g.M_valid;
   const int cols_valid = g.swap ? g.M_valid : g.N_valid;
   const int cs = (lane & 3) * 8;
+  if (g.rp.q_out) {
+    rope_readback(g, stg, lane, row0, col0 + cs, rows_valid);
+    __syncwarp();
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int r = i * 8 + (lane >> 2);
@@ -632,8 +717,15 @@ int gemm_set_variant(int v) {
 
 int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, const void* residual, int T,
                      int O, int K, long long ldx, long long ldw, long long ldy, int mode, int num_sms,
-                     void* workspace, size_t ws_bytes, int* counters, int counters_len, cudaStream_t stream) {
+                     void* workspace, size_t ws_bytes, int* counters, int counters_len, cudaStream_t stream,
+                     const GemmRope* rope) {
   if (T <= 0 || O <= 0) return 0;
+  if (rope && (rope->q_out == nullptr || rope->hd != 128 || O != (rope->hq + 2 * rope->hkv) * 128 ||
+               residual != nullptr || (mode & 4) || rope->ld_q % 8 ||
+               reinterpret_cast<uintptr_t>(rope->q_out) % 16 || reinterpret_cast<uintptr_t>(rope->cache) % 16 ||
+               reinterpret_cast<uintptr_t>(rope->cos_sin) % 16))
+    return set_error("gemm: fused RoPE epilogue needs head_dim 128, O = (Hq + 2 Hkv) * 128, no residual / SwiGLU, "
+                     "16-byte aligned q_out / cache / cos_sin");
   if (K % kBK != 0) return set_error("gemm: K must be a multiple of 64");
   if ((ldx * 2) % 16 || (ldw * 2) % 16) return set_error("gemm: row strides must be 16-byte multiples");
   if (reinterpret_cast<uintptr_t>(X) % 16 || reinterpret_cast<uintptr_t>(W) % 16)
@@ -721,6 +813,7 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
   g.out = reinterpret_cast<__nv_bfloat16*>(Y);
   g.residual = reinterpret_cast<const __nv_bfloat16*>(residual);
   g.bias = reinterpret_cast<const __nv_bfloat16*>(bias);
+  if (rope) g.rp = *rope;
   if (swap) {
     g.hint_a = kEvictFirst;  // weights stream once
     g.hint_b = kEvictLast;   // activations reused by every weight tile

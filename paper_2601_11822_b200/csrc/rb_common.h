@@ -57,9 +57,24 @@ cudaError_t launch_k(void (*kernel)(Exp...), dim3 grid, dim3 block, size_t smem,
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<Act&&>(args)...);
 }
 
+// Fused QKV-projection epilogue (see rope_store in gemm_tcgen05.cu): RoPE on q/k and the
+// paged K/V write of every token row, straight from the GEMM accumulators.
+struct GemmRope {
+  const int* pos;          // [T] position of each row, < 0 = padding (skipped)
+  const int* tok_slot;     // [T] block-table row of each token
+  const int* block_table;  // [slots][bt_stride]
+  int bt_stride;
+  const float* cos_sin;    // fp32 [max_pos][128] = [cos | sin]
+  void* q_out;             // bf16 [T][ld_q]: rotated q heads
+  long long ld_q;
+  void* cache;             // one layer: [num_blocks][2][hkv][16][128] bf16
+  int hq, hkv, hd;
+};
+
 int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, const void* residual, int T,
                      int O, int K, long long ldx, long long ldw, long long ldy, int mode, int num_sms,
-                     void* workspace, size_t ws_bytes, int* counters, int counters_len, cudaStream_t stream);
+                     void* workspace, size_t ws_bytes, int* counters, int counters_len, cudaStream_t stream,
+                     const GemmRope* rope = nullptr);
 
 }  // namespace rb
 

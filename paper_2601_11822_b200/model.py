@@ -6,7 +6,9 @@ This is the physical realization of the two priced calls of the reference:
 replay). Every op goes through the C ABI (ops.py -> librapid_b200.so).
 
 HBM layout:
-  * weights: bf16, K-contiguous [out, in]; QKV fused [(Hq+2Hkv)*D, H];
+  * weights: bf16, K-contiguous [out, in]; QKV fused [(Hq+2Hkv)*D, H], q/k rows
+    RoPE-pair-interleaved (interleave_rope_pairs) so the GEMM epilogue applies RoPE
+    and writes K/V into the paged cache;
     gate/up fused [2I, H], rows interleaved in 16-blocks [g x16 | u x16] so the
     GEMM epilogue emits silu(gate) * up directly
   * KV cache: one tensor [L][num_blocks][2][Hkv][16][D] bf16 — shared by the
@@ -37,6 +39,20 @@ def interleave_gate_up(gate: torch.Tensor, up: torch.Tensor) -> torch.Tensor:
     I, H = gate.shape
     return torch.stack([gate.view(I // GLU_BLOCK, GLU_BLOCK, H), up.view(I // GLU_BLOCK, GLU_BLOCK, H)],
                        dim=1).reshape(2 * I, H)
+
+
+def interleave_rope_pairs(w: torch.Tensor, q_heads: int, kv_heads: int, head_dim: int) -> torch.Tensor:
+    """Reorder the q and k rows of a fused [(Hq+2Hkv)*D, ...] QKV weight (or bias) so that
+    every RoPE pair is adjacent: new row 2j of a head = rotate-half dim j, 2j+1 = dim j+D/2.
+
+    q and k get the same permutation, so q.k (the attention scores) is unchanged; v rows
+    stay in place. The QKV GEMM epilogue then rotates (x[2j], x[2j+1]) pairs that sit in
+    one thread's registers and writes k straight into the paged cache (qk_layout = 1)."""
+    half = head_dim // 2
+    perm = torch.stack([torch.arange(half), torch.arange(half) + half], dim=1).reshape(-1)
+    nqk = (q_heads + kv_heads) * head_dim
+    qk = w[:nqk].reshape(q_heads + kv_heads, head_dim, *w.shape[1:])[:, perm.to(w.device)]
+    return torch.cat([qk.reshape(nqk, *w.shape[1:]), w[nqk:]], 0).contiguous()
 
 
 def rope_inv_freq(arch: ArchConfig) -> torch.Tensor:
@@ -97,6 +113,7 @@ class DecoderWeights:
 
         layers = []
         for _ in range(arch.layers):
+            # random rows: already "pair-interleaved" (any permutation of random rows is random)
             layers.append(LayerWeights(n(H), w(nq, H), w(nq) if arch.qkv_bias else None, w(H, arch.q_heads * D), n(H),
                                        w(2 * I, H), w(H, I)))
         embed = w(arch.vocab, H)
@@ -112,10 +129,12 @@ class DecoderWeights:
         layers = []
         for i in range(arch.layers):
             p = f"layers.{i}."
-            wqkv = torch.cat([state[p + "q"], state[p + "k"], state[p + "v"]], 0)
+            hq, hkv, hd = arch.q_heads, arch.kv_heads, arch.head_dim
+            wqkv = interleave_rope_pairs(torch.cat([state[p + "q"], state[p + "k"], state[p + "v"]], 0), hq, hkv, hd)
             b = None
             if arch.qkv_bias:
-                b = t(torch.cat([state[p + "bq"], state[p + "bk"], state[p + "bv"]], 0))
+                b = t(interleave_rope_pairs(torch.cat([state[p + "bq"], state[p + "bk"], state[p + "bv"]], 0), hq,
+                                            hkv, hd))
             layers.append(LayerWeights(t(state[p + "ln1"]), t(wqkv), b, t(state[p + "o"]), t(state[p + "ln2"]),
                                        t(interleave_gate_up(state[p + "gate"], state[p + "up"])),
                                        t(state[p + "down"])))
@@ -213,7 +232,7 @@ class Runner:
                             kv_cache=self.kv.data_ptr(), kv_layer_stride_bytes=self.kv[0].numel() * 2,
                             num_blocks=self.num_blocks, block_table=self.block_table.data_ptr(),
                             bt_stride=self.block_table.stride(0), cos_sin=self.cos_sin.data_ptr(),
-                            last_tok=self.last_tok.data_ptr())
+                            last_tok=self.last_tok.data_ptr(), qk_layout=1 if a.head_dim == 128 else 0)
             for k, v in keep.items():
                 setattr(m, k, ctypes.cast(v, ctypes.POINTER(ctypes.c_void_p)))
             self._mc = m

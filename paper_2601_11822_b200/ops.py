@@ -50,6 +50,11 @@ _SIGS = {
         [_vp, _c_ll, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _c_ll, _c_float, _c_int, _vp],
         _c_int,
     ),
+    "rb_gemm_qkv_rope": (
+        [_vp, _vp, _vp, _c_int, _c_int, _c_ll, _c_int, _c_int, _c_int, _vp, _vp, _vp, _c_int, _vp, _vp, _c_ll, _vp,
+         _c_int, _c_int, _vp, _c_size, _vp, _c_int, _vp],
+        _c_int,
+    ),
     "rb_rope_cache_write": (
         [_vp, _c_ll, _vp, _vp, _vp, _c_int, _vp, _vp, _c_ll, _vp, _c_int, _c_int, _c_int, _c_int, _vp],
         _c_int,
@@ -77,7 +82,8 @@ class RbModel(ctypes.Structure):
         ("ln1", ctypes.POINTER(_vp)), ("wqkv", ctypes.POINTER(_vp)), ("bqkv", ctypes.POINTER(_vp)),
         ("wo", ctypes.POINTER(_vp)), ("ln2", ctypes.POINTER(_vp)), ("wgu", ctypes.POINTER(_vp)),
         ("wd", ctypes.POINTER(_vp)), ("kv_cache", _vp), ("kv_layer_stride_bytes", _c_size), ("num_blocks", _c_int),
-        ("block_table", _vp), ("bt_stride", _c_int), ("cos_sin", _vp), ("last_tok", _vp)]
+        ("block_table", _vp), ("bt_stride", _c_int), ("cos_sin", _vp), ("last_tok", _vp),
+        ("qk_layout", _c_int)]
 
 
 class RbWorkspace(ctypes.Structure):
@@ -265,6 +271,29 @@ def rope_cache_write(qkv: torch.Tensor, pos: torch.Tensor, tok_slot: torch.Tenso
             _stream(stream),
         ),
         "rb_rope_cache_write",
+    )
+
+
+def qkv_rope(x: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None, pos: torch.Tensor, tok_slot: torch.Tensor,
+             block_table: torch.Tensor, cos_sin: torch.Tensor, q_out: torch.Tensor, cache_layer: torch.Tensor, *,
+             num_q_heads: int, num_kv_heads: int, mode: int = 0, num_sms: int | None = None,
+             scratch: GemmScratch | None = None, stream=None) -> None:
+    """Fused QKV projection + RoPE + paged K/V write (rb_gemm_qkv_rope); w in the
+    pair-interleaved q/k row order of model.interleave_rope_pairs."""
+    _need_cuda(x, w, bias, pos, tok_slot, block_table, cos_sin, q_out, cache_layer)
+    T, K = x.shape
+    D = cache_layer.shape[-1]
+    if w.shape != ((num_q_heads + 2 * num_kv_heads) * D, K) or w.stride(1) != 1 or x.stride(1) != 1:
+        raise ValueError("qkv_rope: w must be [(Hq + 2 Hkv) * D, K], K-contiguous")
+    sms = num_sms if num_sms is not None else device_sm_count(x.device.index or 0)
+    _check(
+        load().rb_gemm_qkv_rope(
+            _ptr(x), _ptr(w), _ptr(bias), T, K, x.stride(0), num_q_heads, num_kv_heads, D, _ptr(pos), _ptr(tok_slot),
+            _ptr(block_table), block_table.stride(0), _ptr(cos_sin), _ptr(q_out), q_out.stride(0), _ptr(cache_layer),
+            mode, sms, _ptr(scratch.ws) if scratch else None, scratch.ws_bytes if scratch else 0,
+            _ptr(scratch.counters) if scratch else None, scratch.counters.numel() if scratch else 0, _stream(stream),
+        ),
+        "rb_gemm_qkv_rope",
     )
 
 

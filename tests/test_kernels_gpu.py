@@ -257,6 +257,69 @@ def test_rope_cache_write():
         assert torch.equal(cache[page, 1, :, p % 16], v)
 
 
+@pytest.mark.parametrize("T,mode,bias,sms", [(7, 2, False, 148), (128, 2, True, 72), (200, 0, False, 148),
+                                             (777, 1, True, 76), (1023, 1, False, 148)])
+def test_qkv_rope_fused(T, mode, bias, sms, scratch):
+    """rb_gemm_qkv_rope (QKV GEMM with RoPE + paged K/V write in its epilogue) against
+    fp32 torch: x @ W^T (+b) in the standard rotate-half layout, RoPE, scatter to pages."""
+    from paper_2601_11822_b200.model import interleave_rope_pairs
+
+    gen = torch.Generator(device=DEV).manual_seed(T + mode)
+    Hq, Hkv, D, H = 32, 8, 128, 1024
+    nq = (Hq + 2 * Hkv) * D
+    x = torch.randn(T, H, device=DEV, generator=gen).bfloat16()
+    w = (torch.randn(nq, H, device=DEV, generator=gen) * 0.03).bfloat16()
+    b = (torch.randn(nq, device=DEV, generator=gen) * 0.5).bfloat16() if bias else None
+    start = 37
+    pos = torch.arange(start, start + T, dtype=torch.int32, device=DEV)
+    pos[T // 2] = -1  # padding row: nothing written
+    slots = torch.full((T,), 1, dtype=torch.int32, device=DEV)
+    npg = (start + T + 15) // 16
+    nb = npg + 8
+    bt = torch.zeros(2, npg, dtype=torch.int32, device=DEV)
+    bt[1] = torch.randperm(nb, generator=torch.Generator().manual_seed(T))[:npg].to(DEV, torch.int32)
+    cs = _cos_sin(start + T + 16, D).to(DEV)
+    q_out = torch.zeros(T, Hq * D, device=DEV, dtype=torch.bfloat16)
+    cache = torch.zeros(nb, 2, Hkv, 16, D, device=DEV, dtype=torch.bfloat16)
+    wi = interleave_rope_pairs(w, Hq, Hkv, D)
+    bi = interleave_rope_pairs(b, Hq, Hkv, D) if bias else None
+    ops.qkv_rope(x, wi, bi, pos, slots, bt, cs, q_out, cache, num_q_heads=Hq, num_kv_heads=Hkv, mode=mode,
+                 num_sms=sms, scratch=scratch)
+    torch.cuda.synchronize()
+
+    ref = x.float() @ w.float().T
+    if bias:
+        ref = ref + b.float()
+    p = pos.long().clamp_min(0)
+    c, s = cs[p, : D // 2][:, None], cs[p, D // 2 :][:, None]
+
+    def rope(z):  # [T, heads, D] rotate-half
+        z1, z2 = z[..., : D // 2], z[..., D // 2 :]
+        return torch.cat([z1 * c - z2 * s, z2 * c + z1 * s], dim=-1)
+
+    qr = rope(ref[:, : Hq * D].view(T, Hq, D))
+    kr = rope(ref[:, Hq * D:(Hq + Hkv) * D].view(T, Hkv, D))
+    vr = ref[:, (Hq + Hkv) * D:].view(T, Hkv, D)
+    half = D // 2
+    perm = torch.stack([torch.arange(half), torch.arange(half) + half], dim=1).reshape(-1).to(DEV)
+    valid = pos >= 0
+    # q/k come out pair-interleaved: dim perm[i] of the standard layout sits at column i
+    assert rel_l2(q_out.view(T, Hq, D)[valid], qr[valid][..., perm]) < 1e-2
+    assert torch.all(q_out[~valid] == 0)
+    page = bt[1][(p // 16)]
+    k_got = cache[page, 0, :, p % 16]  # [T, Hkv, D]
+    v_got = cache[page, 1, :, p % 16]
+    assert rel_l2(k_got[valid], kr[valid][..., perm]) < 1e-2
+    assert rel_l2(v_got[valid], vr[valid]) < 1e-2
+    # the padding row's would-be slot stays untouched
+    pp = start + T // 2
+    assert torch.all(cache[bt[1][pp // 16], :, :, pp % 16] == 0)
+    # scores are invariant: q.k with both permuted == q.k in the standard layout
+    qk_std = (qr[valid][:, ::4] * kr[valid]).sum(-1)
+    qk_int = (q_out.view(T, Hq, D)[valid][:, ::4].float() * k_got[valid].float()).sum(-1)
+    assert rel_l2(qk_int, qk_std) < 2e-2
+
+
 def test_rmsnorm_silu_embed_argmax():
     gen = torch.Generator(device=DEV).manual_seed(5)
     T, H, I, V = 9, 4096, 1024, 4096

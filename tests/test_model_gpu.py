@@ -103,7 +103,12 @@ def test_batched_decode_rows_and_padding(tiny):
         assert int(d.out_ids[i]) == int(torch.argmax(refs[i]))
 
 
-NEAR_TIE = 0.03  # absolute logit gap (logit std ~0.65): below it bf16 rounding may pick either token
+# Absolute logit gap below which bf16 rounding may pick either token. The north-star
+# tolerance (logits rel-L2 <= 2e-2, logit std ~0.65) allows ~0.013 rms error per logit;
+# a flip needs the two top logits to err in opposite directions, so the gap error has
+# rms ~0.018 and 0.05 is ~2.7 sigma of it. Long generations (100+ steps through a bf16
+# KV cache) reach 0.04 occasionally.
+NEAR_TIE = 0.05
 
 
 def teacher_forced_check(orc, prompt, gen):
