@@ -29,6 +29,7 @@ shards by request, no data-path collective), each rank its own trace (seed
 from __future__ import annotations
 
 import argparse
+import collections
 import json
 import math
 import os
@@ -171,6 +172,7 @@ def time_decode_attention(runner, stream, B: int, ctx: int, sms: int, iters: int
 
 
 def main():
+    global PROMPT, OUTPUT
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=600)
@@ -182,13 +184,21 @@ def main():
     ap.add_argument("--duration", type=float, default=None)
     ap.add_argument("--decode-sms", type=int, default=72)
     ap.add_argument("--model", default="llama3.1-8b")
+    ap.add_argument("--prompt", type=int, default=PROMPT, help="mean prompt tokens (cfg 5: 8192)")
+    ap.add_argument("--output", type=int, default=OUTPUT, help="mean output tokens (cfg 5: 128)")
     ap.add_argument("--ref-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--engine", default="rapid", help="rapid | hybrid-<chunk> (same-engine chunked-prefill comparator)")
+    ap.add_argument("--arm-profile", default=None,
+                    help="measured B200 ARM tables (profiler.py JSON); implies --arm with arm.MeasuredArm")
+    ap.add_argument("--arm-policy", default="balanced", choices=["balanced", "slo-min"])
     ap.add_argument("--arm", action="store_true",
                     help="cfg 3: adaptive ARM (allocate() per launch) instead of the cfg-2 static split")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    PROMPT, OUTPUT = args.prompt, args.output
+    if args.arm_profile:
+        args.arm = True
 
     rank, world, local = dist_setup()
     if args.impl == "reference":
@@ -224,7 +234,14 @@ def main():
     else:
         ex = B200Executor(arch, seed=rank, static_decode_sms=None if args.arm else args.decode_sms, max_batch=256,
                           chunk_tokens=2048, max_context=PROMPT + OUTPUT + 64, num_slots=1024)
-    ex.warmup()
+    policy = None
+    if args.arm_profile and not hybrid:
+        from paper_2601_11822_b200.arm import MeasuredArm, MeasuredProfile
+
+        policy = MeasuredArm(MeasuredProfile.load(args.arm_profile), SLO_ITL_US, 256, args.arm_policy)
+        ex.warmup(sorted(policy.splits_used(), key=lambda d: -1 if d is None else d))
+    else:
+        ex.warmup()
     pkey = None if args.arm else args.decode_sms
     d_sms = ex._partitions[pkey].d_sms
     p_sms = ex._partitions[pkey].p_sms
@@ -236,7 +253,8 @@ def main():
         engine = HybridEngine(model, b200_spec(), CostParams(), slo, chunk_tokens=hchunk, max_batch=256, executor=ex)
     else:
         engine = RapidEngine(model, b200_spec(), CostParams(), slo, chunk_tokens=2048, max_batch=256, executor=ex,
-                             static_decision=None if args.arm else static, record_decisions=args.arm)
+                             static_decision=None if args.arm else static, record_decisions=args.arm,
+                             arm_policy=policy)
 
     # ---- timed window over decode steps, hooked on the executor
     horizon = int(duration * 1e6)
@@ -344,10 +362,12 @@ def main():
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "bf16",
-        "data": "synthetic (random-init Llama-3.1-8B weights, synthesize() trace)",
+        "data": f"synthetic (random-init {args.model} weights of the real shapes, synthesize() trace)",
         "config": {
-            "workload": (f"cfg3: {args.model} bf16, adaptive ARM (allocate() at every launch; OVERALLOCATE -> "
-                         f"both phases on {total} SMs, PARTITION -> green-context split)" if args.arm else
+            "workload": (f"cfg3: {args.model} bf16, adaptive ARM ("
+                         + (f"measured B200 tables, {args.arm_policy} policy" if policy else "reference allocate()")
+                         + f" at every launch; OVERALLOCATE -> both phases on {total} SMs, PARTITION -> "
+                           f"green-context split)" if args.arm else
                          f"cfg2: {args.model} bf16, 1x B200 per replica, static split decode {d_sms} / prefill "
                          f"{p_sms} SMs") + f", trace in {PROMPT}/out {OUTPUT} sigma=0 at {args.qps} QPS for "
                                          f"{duration:.0f} s",
@@ -379,8 +399,12 @@ def main():
         "clocks": win.get("clocks", {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}),
         "cpu_baseline": cpu,
         "run_wall_s": t_run,
-        "arm_decisions": ({k: sum(1 for _, d in engine.decision_log if d.mode.value == k)
-                           for k in ("overallocate", "partition")} if getattr(engine, "decision_log", None) else None),
+        "arm_decisions": ({**{k: sum(1 for _, d in engine.decision_log if d.mode.value == k)
+                              for k in ("overallocate", "partition")},
+                           "decode_sms": dict(sorted(collections.Counter(
+                               str(round(d.cu_fraction_decode * total)) for _, d in engine.decision_log
+                               if d.mode.value == "partition").items()))}
+                          if getattr(engine, "decision_log", None) else None),
         "requests": len(engine.requests),
         "finished": sum(1 for r in engine.requests if r.state.value == "finished"),
         "profiles": profile_path,

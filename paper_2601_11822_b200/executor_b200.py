@@ -251,7 +251,7 @@ class B200Executor:
                 self._pre_ids_dev[:n].copy_(self._pre_ids_host[:n], non_blocking=True)
                 self.runner.prefill(slot, self._pre_ids_dev[:n], lo, num_sms=part.p_sms, stream=sh)
             self.h2d_bytes += 4 * n
-            self.gpu_launches += 2 + 9 * self.arch.layers
+            self.gpu_launches += self.runner.kernels_per_forward(0, n, False, False, False)
         if written + chunk == target:
             nxt = int(self._context_ids(req, target - 1, target)[0])
             ops.set_last_token(self.runner.last_tok, slot, value=nxt, stream=sh)
@@ -339,7 +339,7 @@ class B200Executor:
         self.h2d_bytes += 12 * bucket
         self.d2h_bytes += 4 * B
         self.decode_steps += 1
-        self.gpu_launches += 4 + 9 * self.arch.layers + 3
+        self.gpu_launches += self.runner.kernels_per_forward(bucket, 0, True, False, True)
         return h
 
     def finish_decode(self, handle) -> None:
@@ -448,7 +448,7 @@ class HybridB200Executor(B200Executor):
         self.h2d_bytes += 12 * B + 4 * chunk
         self.d2h_bytes += 4 * (B + (1 if emit else 0))
         self.decode_steps += 1
-        self.gpu_launches += 2 + 9 * self.arch.layers + 4
+        self.gpu_launches += self.runner.kernels_per_forward(B, chunk if chunk_dev is not None else 0, True, emit, True)
         return h
 
     def finish_hybrid(self, handle) -> None:

@@ -250,6 +250,21 @@ class Runner:
                                gemm_counters_len=B.scratch.counters.numel(), attn_ws=self.attn_ws.data_ptr(),
                                attn_ws_bytes=self.attn_ws.numel() * 4)
 
+    def kernels_per_forward(self, n_decode: int, n_prefill: int, logits_decode: bool, emit_prefill: bool,
+                            sample: bool) -> int:
+        """Kernel launches of one rb_decoder_forward call (mirrors csrc/forward.cu)."""
+        T = n_decode + n_prefill
+        if T == 0:
+            return 0
+        fused_rope = self.arch.head_dim == 128
+        per_layer = (2 + (0 if fused_rope else 1) + int(n_decode > 0) + int(n_prefill > 0) + 2
+                     + (1 if T > 256 else 2))
+        n = int(n_decode > 0) + int(n_prefill > 0) + self.arch.layers * per_layer
+        nl = (n_decode if logits_decode else 0) + (1 if emit_prefill and n_prefill else 0)
+        if nl:
+            n += int(bool(logits_decode and n_decode)) + int(bool(emit_prefill and n_prefill)) + 1 + int(sample)
+        return n
+
     # ------------------------------------------------------------------ prefill
     def prefill(self, slot: int, token_ids: torch.Tensor, start: int, *, num_sms: int, stream=None,
                 logits: bool = False) -> torch.Tensor | None:

@@ -1,0 +1,153 @@
+"""Measured B200 ARM profile (the `pdsim profile` step).
+
+The reference's offline profiler (`pdsim profile`, cli.py:99-110; build_profile,
+costmodel.py:301-335) *predicts* the smallest CU fraction whose contended decode
+step fits margin x SLO for every batch of DEFAULT_BATCH_GRID. Here the same table
+is MEASURED on the device: for every decode partition on the 8-SM green-context
+ladder and every batch, one CUDA-graph decode step (all layers + lm_head +
+argmax, the step RAPID launches) is timed on the decode green context while a
+prefill chunk stream keeps the complementary partition busy. The prefill side's
+chunk time under that load is recorded too, so a policy can trade decode
+latency against prefill throughput.
+
+    python -m paper_2601_11822_b200.profiler --model llama3.1-8b --ctx 1152 --out profiles/arm_llama8b.json
+
+The JSON holds {"decode_us": {D: {B: us}}, "overalloc_decode_us": {B: us},
+"prefill_us_per_token": {D: us}, ...}; `MeasuredProfile` (arm.py) reads it and
+writes the reference's interchange lines `batch,fraction[,saturated]`.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import statistics
+import time
+
+import torch
+
+from paper_2601_11822_b200 import ops
+from paper_2601_11822_b200.arm import DEFAULT_BATCH_GRID
+from paper_2601_11822_b200.model import PAGE, DecoderWeights, Runner
+from paper_2601_11822_b200.specs import ARCHS, SM_GRANULARITY
+
+DEFAULT_LADDER = (16, 24, 32, 40, 48, 56, 64, 72, 88, 104, 120, 136)
+
+
+def _med(xs):
+    return statistics.median(xs)
+
+
+def measure(model: str = "llama3.1-8b", ctx: int = 1152, chunk: int = 2048, ladder=DEFAULT_LADDER,
+            batches=DEFAULT_BATCH_GRID, reps: int = 3, steps: int = 4, log=print) -> dict:
+    arch = ARCHS[model]
+    torch.cuda.set_device(0)
+    ops.load()
+    total = ops.device_sm_count(0)
+    Bmax = max(batches)
+    w = DecoderWeights.random(arch, device="cuda")
+    nbps = (max(ctx, chunk) + PAGE) // PAGE + 1
+    nblocks = Bmax * nbps + nbps + 8
+    r = Runner(w, nblocks, Bmax + 1, nbps, max_prefill_tokens=chunk, max_decode_batch=Bmax)
+    r.kv.normal_(std=0.5)
+    r.block_table[:Bmax] = torch.arange(Bmax * nbps, dtype=torch.int32, device="cuda").view(Bmax, nbps)
+    r.block_table[Bmax] = torch.arange(Bmax * nbps, Bmax * nbps + nbps, dtype=torch.int32, device="cuda")
+    d = r.dec
+    d.slot[:Bmax] = torch.arange(Bmax, dtype=torch.int32, device="cuda")
+    d.pos[:Bmax] = ctx - 1
+    d.seq[:Bmax] = ctx
+    ids = torch.randint(0, arch.vocab, (chunk,), dtype=torch.int32, device="cuda")
+    mp = (ctx + PAGE - 1) // PAGE
+    out = {"model": model, "ctx": ctx, "chunk": chunk, "total_sms": total, "granularity": SM_GRANULARITY,
+           "batches": list(batches), "decode_us": {}, "prefill_us_per_token": {}, "prefill_alone_us_per_token": {},
+           "overalloc_decode_us": {}, "overalloc_prefill_us_per_token": None}
+
+    def run_partition(ds, ps, d_sms, p_sms):
+        def prefill_chunk():
+            with torch.cuda.stream(ps):
+                r.prefill(Bmax, ids, 0, num_sms=p_sms, stream=ps.cuda_stream)
+
+        # prefill alone (its chunk time sets how many chunks cover a decode window)
+        prefill_chunk()
+        torch.cuda.synchronize()
+        pts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(ps)
+            prefill_chunk()
+            b.record(ps)
+            ps.synchronize()
+            pts.append(a.elapsed_time(b) * 1e3)
+        p_alone = _med(pts)
+        dec, pre_conc = {}, []
+        for B in batches:
+            with torch.cuda.stream(ds):
+                r.decode_body(B, num_sms=d_sms, max_pages=mp, stream=ds.cuda_stream)
+            ds.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=ds):
+                r.decode_body(B, num_sms=d_sms, max_pages=mp, stream=ds.cuda_stream)
+            ds.synchronize()
+            g.replay()
+            ds.synchronize()
+            dts = []
+            for _ in range(reps):
+                torch.cuda.synchronize()
+                # keep the prefill partition busy for the whole decode window: chunks are
+                # queued first; the decode events bracket replays that start once it runs
+                n_chunks = 1 + int(steps * (dts[-1] if dts else 20_000.0) * 1.5 / max(p_alone, 1.0))
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(ps)
+                for _ in range(min(n_chunks, 16)):
+                    prefill_chunk()
+                b.record(ps)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(ds):
+                    e0.record(ds)
+                    for _ in range(steps):
+                        g.replay()
+                    e1.record(ds)
+                torch.cuda.synchronize()
+                dts.append(e0.elapsed_time(e1) * 1e3 / steps)
+                pre_conc.append(a.elapsed_time(b) * 1e3 / min(n_chunks, 16))
+            dec[B] = round(_med(dts), 1)
+            del g
+        return dec, _med(pre_conc) / chunk, p_alone / chunk
+
+    for D in ladder:
+        t0 = time.perf_counter()
+        gs = ops.GreenSplit(D)
+        ds, ps = gs.streams
+        dec, p_tok, p_alone_tok = run_partition(ds, ps, gs.sms[0], gs.sms[1])
+        out["decode_us"][str(gs.sms[0])] = dec
+        out["prefill_us_per_token"][str(gs.sms[0])] = round(p_tok, 3)
+        out["prefill_alone_us_per_token"][str(gs.sms[0])] = round(p_alone_tok, 3)
+        log(f"decode {gs.sms[0]:3d} SMs / prefill {gs.sms[1]:3d}: prefill {p_tok:.2f} us/token under load "
+            f"({p_alone_tok:.2f} alone); decode us {dec}  [{time.perf_counter() - t0:.1f} s]")
+    # OVERALLOCATE: both phases on the whole device, two ordinary streams
+    ds, ps = torch.cuda.Stream(), torch.cuda.Stream()
+    dec, p_tok, p_alone_tok = run_partition(ds, ps, total, total)
+    out["overalloc_decode_us"] = dec
+    out["overalloc_prefill_us_per_token"] = round(p_tok, 3)
+    out["full_prefill_alone_us_per_token"] = round(p_alone_tok, 3)
+    log(f"overallocate: prefill {p_tok:.2f} us/token under load ({p_alone_tok:.2f} alone); decode us {dec}")
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--model", default="llama3.1-8b")
+    ap.add_argument("--ctx", type=int, default=1152)
+    ap.add_argument("--chunk", type=int, default=2048)
+    ap.add_argument("--ladder", default=",".join(map(str, DEFAULT_LADDER)))
+    ap.add_argument("--batches", default=",".join(map(str, DEFAULT_BATCH_GRID)))
+    ap.add_argument("--out", required=True)
+    args = ap.parse_args()
+    res = measure(args.model, args.ctx, args.chunk, tuple(int(x) for x in args.ladder.split(",")),
+                  tuple(int(x) for x in args.batches.split(",")))
+    with open(args.out, "w") as fh:
+        json.dump(res, fh, indent=1)
+
+
+if __name__ == "__main__":
+    main()

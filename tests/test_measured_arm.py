@@ -1,0 +1,88 @@
+"""Measured-table ARM (arm.MeasuredProfile / MeasuredArm) on a synthetic profile.
+
+The tables mimic profiler.py output: decode step time falls with decode SMs and
+grows with batch; the prefill side's per-token time grows as decode takes SMs.
+"""
+
+import pytest
+
+from paper_2601_11822_b200.arm import (DEFAULT_BATCH_GRID, MeasuredArm, MeasuredProfile, decode_sms_of,
+                                       profile_lines)
+from paper_2601_11822_b200.specs import AllocationMode
+
+LADDER = (16, 24, 32, 40, 48, 56, 64, 72, 88, 104, 120, 136)
+
+
+def synth(total=148):
+    dec, pre = {}, {}
+    for d in LADDER:
+        # weights 15 ms-equivalent at 16 SMs shrinking with SMs; KV term linear in batch
+        dec[str(d)] = {str(b): round((3000 + 60 * b) * 72 / min(d, 96), 1) for b in DEFAULT_BATCH_GRID}
+        pre[str(d)] = round(20.0 * 76 / (total - d), 3)
+    return {"model": "synthetic", "ctx": 1152, "chunk": 2048, "total_sms": total, "granularity": 8,
+            "batches": list(DEFAULT_BATCH_GRID), "decode_us": dec, "prefill_us_per_token": pre,
+            "overalloc_decode_us": {str(b): round(1.6 * (3000 + 60 * b), 1) for b in DEFAULT_BATCH_GRID},
+            "overalloc_prefill_us_per_token": 14.0}
+
+
+def test_profile_lines_match_reference_format():
+    mp = MeasuredProfile(synth())
+    prof = mp.to_profile(50_000)
+    lines = profile_lines(prof)
+    assert len(lines) == len(DEFAULT_BATCH_GRID)
+    for ln, b in zip(lines, DEFAULT_BATCH_GRID):
+        parts = ln.split(",")
+        assert int(parts[0]) == b
+        frac = float(parts[1])
+        # smallest ladder partition whose step fits 0.9 x SLO
+        want = next((d for d in LADDER if mp.decode_us(d, b) <= 45_000), None)
+        if want is None:
+            assert parts[2] == "saturated"
+        else:
+            assert abs(frac - want / 148) < 1e-6
+
+
+def test_idle_phase_overallocates():
+    arm = MeasuredArm(MeasuredProfile(synth()), 50_000)
+    assert arm.decide(0, 4096, 0.25).mode is AllocationMode.OVERALLOCATE
+    assert arm.decide(128, 0, 0.25).mode is AllocationMode.OVERALLOCATE
+
+
+def test_balanced_split_meets_slo_and_balances():
+    mp = MeasuredProfile(synth())
+    arm = MeasuredArm(mp, 50_000, max_batch=256, policy="balanced")
+    for b in (16, 64, 128, 256):
+        d = decode_sms_of(arm.decide(b, 2048, 0.25), 148)
+        assert mp.decode_us(d, b) <= 45_000
+    # more output per prompt token -> decode side needs more SMs (never fewer)
+    lo = decode_sms_of(arm.decide(128, 2048, 0.05), 148)
+    hi = decode_sms_of(arm.decide(128, 2048, 1.0), 148)
+    lo_v = 148 if lo is None else lo
+    hi_v = 148 if hi is None else hi
+    assert lo_v <= hi_v
+
+
+def test_slo_min_is_reference_rule():
+    mp = MeasuredProfile(synth())
+    arm = MeasuredArm(mp, 50_000, policy="slo-min")
+    prof = mp.to_profile(50_000)
+    for b in DEFAULT_BATCH_GRID:
+        dec = arm.decide(b, 1024, 0.25)
+        if mp.decode_us(None, b) <= 50_000:
+            assert dec.mode is AllocationMode.OVERALLOCATE
+        else:
+            e = prof.lookup(b)
+            assert dec.mode is AllocationMode.PARTITION
+            assert decode_sms_of(dec, 148) == (LADDER[-1] if e.saturated else round(e.cu_fraction * 148))
+
+
+def test_splits_used_covers_decisions():
+    arm = MeasuredArm(MeasuredProfile(synth()), 50_000)
+    used = arm.splits_used()
+    for b in DEFAULT_BATCH_GRID:
+        assert decode_sms_of(arm.decide(b, 1, 0.25), 148) in used
+
+
+def test_bad_policy():
+    with pytest.raises(ValueError):
+        MeasuredArm(MeasuredProfile(synth()), 50_000, policy="nope")
