@@ -278,7 +278,8 @@ def main():
         if st["start_handle"] is not None and st["end_handle"] is None:
             st["steps"] += 1
             st["Bs"].append(len(members))
-            st["ctxs"].append(sum(r.context_tokens for r in members) / len(members))
+            if members:
+                st["ctxs"].append(sum(r.context_tokens for r in members) / len(members))
             h._win = True
             if st["steps"] == args.steps:
                 st["end_handle"] = h
@@ -339,6 +340,19 @@ def main():
     h2d = (win["h2d1"] - win["h2d0"]) / steps if complete else 0
     d2h = (win["d2h1"] - win["d2h0"]) / steps if complete else 0
     launches = int(win["launch1"] - win["launch0"]) if complete else 0
+
+    # duty cycles over the window: device-busy time / wall time between launches on each phase stream
+    def duty(log, t0, t1):
+        sel = [(g, ns) for g, ns in log if t0 <= ns <= t1]
+        if len(sel) < 2:
+            return None
+        span_us = (sel[-1][1] - sel[0][1]) / 1e3
+        return round(sum(g for g, _ in sel[:-1]) / span_us, 3) if span_us > 0 else None
+
+    w0 = getattr(win["start_handle"], "launch_ns", 0) if complete else 0
+    w1 = getattr(win["end_handle"], "launch_ns", 0) if complete else 0
+    duties = {"decode": duty([(g, ns) for _, g, ns in ex.step_log], w0, w1),
+              "prefill": duty(getattr(ex, "prefill_log", []), w0, w1)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -405,6 +419,7 @@ def main():
                                str(round(d.cu_fraction_decode * total)) for _, d in engine.decision_log
                                if d.mode.value == "partition").items()))}
                           if getattr(engine, "decision_log", None) else None),
+        "stream_duty": duties,
         "requests": len(engine.requests),
         "finished": sum(1 for r in engine.requests if r.state.value == "finished"),
         "profiles": profile_path,

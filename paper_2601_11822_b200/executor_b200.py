@@ -142,6 +142,7 @@ class B200Executor:
         self.prefill_chunks = 0
         self.gpu_launches = 0
         self.step_log: list[tuple[int, int, int]] = []  # (B, gpu_us, host launch ns)
+        self.prefill_log: list[tuple[int, int]] = []  # (gpu_us, host launch ns)
 
     # ------------------------------------------------------------------ sizing
     def _activation_bytes(self, T: int, B: int) -> int:
@@ -262,7 +263,8 @@ class B200Executor:
         return h
 
     def finish_prefill(self, handle) -> None:
-        pass
+        if handle is not None:
+            self.prefill_log.append((handle.gpu_us, handle.launch_ns))
 
     # ------------------------------------------------------------------ decode
     def _bucket(self, B: int) -> int:

@@ -44,9 +44,14 @@ def measure(model: str = "llama3.1-8b", ctx: int = 1152, chunk: int = 2048, ladd
     torch.cuda.set_device(0)
     ops.load()
     total = ops.device_sm_count(0)
-    Bmax = max(batches)
     w = DecoderWeights.random(arch, device="cuda")
     nbps = (max(ctx, chunk) + PAGE) // PAGE + 1
+    # batches whose KV fits next to the weights (long contexts cap the batch, as the pool would)
+    free, _ = torch.cuda.mem_get_info()
+    per_seq = nbps * Runner.kv_bytes_per_block(arch)
+    cap = int((free - (12 << 30)) // per_seq) - 1
+    batches = tuple(b for b in batches if b <= cap) or (max(1, cap),)
+    Bmax = max(batches)
     nblocks = Bmax * nbps + nbps + 8
     r = Runner(w, nblocks, Bmax + 1, nbps, max_prefill_tokens=chunk, max_decode_batch=Bmax)
     r.kv.normal_(std=0.5)

@@ -1,0 +1,80 @@
+"""Decode GEMMs as they run inside a decode step: a CUDA-graph chain of N launches, each on a
+different weight matrix (so every launch streams its weights from HBM), PDL on.
+
+    python scripts/gemm_chain.py [--sms 72] [--batches 32,128,256] [--n 8]
+
+Prints per-launch us and weight TB/s for our kernel and for cuBLAS (torch.matmul) in the
+same chain shape, on the same green-context partition.
+"""
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2601_11822_b200 import ops  # noqa: E402
+
+SHAPES = {"qkv": (6144, 4096), "o": (4096, 4096), "gate_up": (28672, 4096), "down": (4096, 14336)}
+
+
+def chain_time(fn_list, stream, reps=5):
+    with torch.cuda.stream(stream):
+        for f in fn_list:
+            f()
+    stream.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for f in fn_list:
+            f()
+    ts = []
+    with torch.cuda.stream(stream):
+        g.replay()
+        stream.synchronize()
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            g.replay()
+            b.record(stream)
+            stream.synchronize()
+            ts.append(a.elapsed_time(b) * 1e3)
+    ts.sort()
+    return ts[len(ts) // 2]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sms", type=int, default=72)
+    ap.add_argument("--batches", default="32,128,256")
+    ap.add_argument("--n", type=int, default=8)
+    ap.add_argument("--shapes", default="qkv,o,gate_up,down")
+    ap.add_argument("--variant", type=int, default=-1)
+    args = ap.parse_args()
+    lib = ops.load()
+    lib.rb_debug_gemm_variant(args.variant)
+    if args.sms >= 148:
+        st, sms = torch.cuda.Stream(), 148
+    else:
+        gs = ops.GreenSplit(args.sms)
+        st, sms = gs.streams[0], gs.sms[0]
+    sc = ops.GemmScratch("cuda")
+    for name in args.shapes.split(","):
+        O, K = SHAPES[name]
+        ws = [(torch.randn(O, K, device="cuda") * 0.02).bfloat16() for _ in range(args.n)]
+        for B in [int(b) for b in args.batches.split(",")]:
+            x = torch.randn(B, K, device="cuda").bfloat16()
+            y = torch.empty(B, O, device="cuda", dtype=torch.bfloat16)
+            ours = [lambda w=w: ops.linear(x, w, out=y, mode=2, num_sms=sms, scratch=sc, stream=st) for w in ws]
+            cub = [lambda w=w: torch.matmul(x, w.t(), out=y) for w in ws]
+            t_ours = chain_time(ours, st) / args.n
+            t_cub = chain_time(cub, st) / args.n
+            wb = O * K * 2
+            print(json.dumps({"shape": name, "B": B, "sms": sms, "us": round(t_ours, 2),
+                              "tbs": round(wb / t_ours / 1e6, 2), "cublas_us": round(t_cub, 2),
+                              "cublas_tbs": round(wb / t_cub / 1e6, 2)}), flush=True)
+        del ws
+
+
+if __name__ == "__main__":
+    main()
