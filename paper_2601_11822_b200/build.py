@@ -26,7 +26,9 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxe
 
 
 def lib_path() -> Path:
-    return OUT_DIR / LIB_NAME
+    """The in-tree library (RB_LIB overrides it: A/B runs of two builds on the GPU box)."""
+    env = os.environ.get("RB_LIB")
+    return Path(env) if env else OUT_DIR / LIB_NAME
 
 
 def _sources() -> list[Path]:

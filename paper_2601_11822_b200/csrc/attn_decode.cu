@@ -176,16 +176,22 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     for (int p = p0; p < p1; ++p) {
       mbar_wait(&bars[stage], phase);
       const uint32_t base = smem_u32(ring + (size_t)stage * kStageBytes);
-      // ---- S^T = K Q^T
+      // ---- S^T = K Q^T: even / odd k-steps into two accumulators (halves the MMA
+      // dependency chain on the critical path of every page)
       float s[4] = {0.f, 0.f, 0.f, 0.f};
+      float s2[4] = {0.f, 0.f, 0.f, 0.f};
       const int mi = lane >> 3;
       const int rr = (mi & 1) * 8 + (lane & 7);
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        uint32_t a0, a1, a2, a3;
+      for (int kk = 0; kk < 8; kk += 2) {
+        uint32_t a0, a1, a2, a3, c0, c1, c2, c3;
         ldsm_x4(base + pg_off(rr, 2 * kk + (mi >> 1)), a0, a1, a2, a3);
+        ldsm_x4(base + pg_off(rr, 2 * kk + 2 + (mi >> 1)), c0, c1, c2, c3);
         mma_bf16_16816(s, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
+        mma_bf16_16816(s2, c0, c1, c2, c3, qb[kk + 1][0], qb[kk + 1][1]);
       }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) s[e] += s2[e];
       // ---- mask + online softmax (columns = heads 2t, 2t+1; rows = tokens g, g+8)
       const int tok0 = p * kPage + g;
       float s00 = s[0] * a.scale_log2, s01 = s[1] * a.scale_log2;

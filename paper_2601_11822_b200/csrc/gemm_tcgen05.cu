@@ -64,6 +64,7 @@ struct GemmArgs {
   float* ws;      // stream-K partials [cluster][rank][mt][BN/32][4 warps][8][32 lanes] float4
   int* counters;  // per (tile, rank), self-resetting
   GemmRope rp;    // rp.q_out != nullptr: fused RoPE + paged K/V write epilogue (QKV projection)
+  unsigned long long* trace;  // debug timeline: [cta][8] globaltimer stamps of this launch, or null
 };
 
 // Work schedule shared by the producer, MMA and epilogue roles. Data-parallel: whole
@@ -110,8 +111,11 @@ struct SegIter {
   }
 };
 
-// Optional timeline trace (debug): per CTA 8 globaltimer stamps.
-__device__ unsigned long long* g_gemm_trace = nullptr;
+// Optional timeline trace (debug): per CTA 16 globaltimer stamps; consecutive launches
+// after rb_debug_gemm_trace(buf) go to buf + (i % 16) * 148 * 16 (absolute times, so a
+// chain of PDL-overlapped launches can be laid side by side).
+static unsigned long long* g_trace_host = nullptr;
+static unsigned g_trace_launch = 0;
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -121,7 +125,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 // pipelined loops would be re-issued every k-block (the barrier asm clobbers memory).
 #define TRACE(slot)                                           \
   do {                                                        \
-    if (trace) trace[blockIdx.x * 8 + (slot)] = gtime();     \
+    if (trace) trace[blockIdx.x * 16 + (slot)] = gtime();    \
   } while (0)
 
 // Fused QKV epilogue readback: this lane's 8 columns [col, col+8) of 4 token rows.
@@ -204,8 +208,44 @@ __device__ __forceinline__ void rope_readback(const GemmArgs& g, const __nv_bflo
 }
 
 // One warp's 32 (MMA rows) x 32 (MMA cols) accumulator block -> Y.
+// The residual / bias vectors this lane adds come preloaded (epi_preload), all four rows
+// at once and one 32-column chunk ahead: R may alias Y (in-place residual), so loads
+// interleaved with the stores would serialize into dependent L2 round trips.
+struct EpiPre {
+  uint4 rr[4];  // residual, rows i*8 + lane/4
+  uint4 bb;     // bias
+};
+
+__device__ __forceinline__ void epi_preload(const GemmArgs& g, int lane, int m0, int n0, EpiPre& pre) {
+  const int row0 = g.swap ? n0 : m0;
+  const int col = (g.swap ? m0 : n0) + (lane & 3) * 8;
+  const int rows_valid = g.swap ? g.N_valid : g.M_valid;
+  const int cols_valid = g.swap ? g.M_valid : g.N_valid;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) pre.rr[i] = make_uint4(0, 0, 0, 0);
+  pre.bb = make_uint4(0, 0, 0, 0);
+  if (g.rp.q_out || g.glu || col + 8 > cols_valid) return;
+  if (g.bias) pre.bb = *reinterpret_cast<const uint4*>(g.bias + col);
+  if (g.residual) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int row = row0 + i * 8 + (lane >> 2);
+      if (row < rows_valid) pre.rr[i] = *reinterpret_cast<const uint4*>(g.residual + (long long)row * g.ldy + col);
+    }
+  }
+}
+
 __device__ __forceinline__ void epi_block(const GemmArgs& g, __nv_bfloat16* stg, int lane, int m0, int n0,
-                                          const uint32_t (&v)[32]) {
+                                          const uint32_t (&v)[32], const EpiPre& pre, bool tstamp = false) {
+  const int row0 = g.swap ? n0 : m0;  // output row (token) base
+  const int col0 = g.swap ? m0 : n0;  // output col (feature) base
+  const int rows_valid = g.swap ? g.N_valid : g.M_valid;
+  const int cols_valid = g.swap ? g.M_valid : g.N_valid;
+  const int cs = (lane & 3) * 8;
+  const int col = col0 + cs;
+  const bool vec = col + 8 <= cols_valid;
+  const uint4* rr = pre.rr;
+  const uint4 bb = pre.bb;
   if (!g.swap) {
     uint4* dst = reinterpret_cast<uint4*>(stg + lane * kStgStride);
 #pragma unroll
@@ -220,13 +260,9 @@ __device__ __forceinline__ void epi_block(const GemmArgs& g, __nv_bfloat16* stg,
     for (int j = 0; j < 32; ++j) stg[j * kStgStride + lane] = __float2bfloat16_rn(__uint_as_float(v[j]));
   }
   __syncwarp();
-  const int row0 = g.swap ? n0 : m0;  // output row (token) base
-  const int col0 = g.swap ? m0 : n0;  // output col (feature) base
-  const int rows_valid = g.swap ? g.N_valid : g.M_valid;
-  const int cols_valid = g.swap ? g.M_valid : g.N_valid;
-  const int cs = (lane & 3) * 8;
+  if (tstamp && lane == 0 && g.trace) g.trace[blockIdx.x * 16 + 15] = gtime();
   if (g.rp.q_out) {
-    rope_readback(g, stg, lane, row0, col0 + cs, rows_valid);
+    rope_readback(g, stg, lane, row0, col, rows_valid);
     __syncwarp();
     return;
   }
@@ -234,7 +270,6 @@ __device__ __forceinline__ void epi_block(const GemmArgs& g, __nv_bfloat16* stg,
   for (int i = 0; i < 4; ++i) {
     const int r = i * 8 + (lane >> 2);
     const int row = row0 + r;
-    const int col = col0 + cs;
     if (row >= rows_valid || col >= cols_valid) continue;
     const uint4 sv = *reinterpret_cast<const uint4*>(stg + r * kStgStride + cs);
     float x[8];
@@ -248,10 +283,13 @@ __device__ __forceinline__ void epi_block(const GemmArgs& g, __nv_bfloat16* stg,
       }
     }
     __nv_bfloat16* dst = g.out + (long long)row * g.ldy + col;
-    if (col + 8 <= cols_valid) {
+    if (g.dbg & 4) {
+      if (x[0] == 12345.f) dst[0] = __float2bfloat16_rn(x[1]);  // keep the math alive
+      continue;
+    }
+    if (vec) {
       if (g.bias) {
-        const uint4 b = *reinterpret_cast<const uint4*>(g.bias + col);
-        const uint32_t w[4] = {b.x, b.y, b.z, b.w};
+        const uint32_t w[4] = {bb.x, bb.y, bb.z, bb.w};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           float2 f = unpack_bf16x2(w[j]);
@@ -260,8 +298,7 @@ __device__ __forceinline__ void epi_block(const GemmArgs& g, __nv_bfloat16* stg,
         }
       }
       if (g.residual) {
-        const uint4 rr = *reinterpret_cast<const uint4*>(g.residual + (long long)row * g.ldy + col);
-        const uint32_t w[4] = {rr.x, rr.y, rr.z, rr.w};
+        const uint32_t w[4] = {rr[i].x, rr[i].y, rr[i].z, rr[i].w};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           float2 f = unpack_bf16x2(w[j]);
@@ -285,7 +322,9 @@ __device__ __forceinline__ void epi_block(const GemmArgs& g, __nv_bfloat16* stg,
 
 // SwiGLU epilogue: the 32 accumulator columns (normal) / rows (swap) of a block are
 // [gate f..f+15 | up f..f+15] for 16 output features f = (block start) / 2.
-__device__ __forceinline__ float silu_mul_f(float gt, float up) { return gt / (1.f + __expf(-gt)) * up; }
+__device__ __forceinline__ float silu_mul_f(float gt, float up) {
+  return __fdividef(gt, 1.f + __expf(-gt)) * up;  // MUFU ex2 + rcp, no IEEE-division slow path
+}
 
 __device__ __forceinline__ void epi_block_glu(const GemmArgs& g, __nv_bfloat16* stg, int lane, int m0, int n0,
                                               const uint32_t (&v)[32]) {
@@ -352,7 +391,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
                              const __grid_constant__ CUtensorMap tmap_b, const GemmArgs g) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment by pointer arithmetic on the __shared__ array (an integer round
+  // trip would drop the address space: every staging access would compile to generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int BN = g.BN;
   const int stages = g.stages;
   constexpr int MT = kMT;
@@ -368,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty = tfull + 2;      // 2
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-  unsigned long long* const trace = g_gemm_trace;
+  unsigned long long* const trace = g.trace;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = (kPair == 2) ? cluster_ctarank() : 0u;
@@ -568,12 +609,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int m0 = mbase + i * kBM * kPair;
           if (m0 >= g.M_valid) continue;
           for (int c = 0; c < BN; c += 32) {
+            EpiPre pre;
+            epi_preload(g, lane, m0, nt * BN + c, pre);
             uint32_t v[32];
+            if (lane == 0 && q == 0 && first && i == 0 && c < 64) TRACE(11 + (c >> 5));
             tmem_ld_sum(tbase + (uint32_t)(i * BN + c), KA, sub_stride, v);
+            if (lane == 0 && q == 0 && first && i == 0 && c == 32) TRACE(13);
             if (nt * BN + c < g.N_valid) {
               if (g.glu) epi_block_glu(g, stg, lane, m0, nt * BN + c, v);
-              else epi_block(g, stg, lane, m0, nt * BN + c, v);
+              else epi_block(g, stg, lane, m0, nt * BN + c, v, pre, lane == 0 && q == 0 && first && i == 0 && c == 32);
             }
+            if (lane == 0 && q == 0 && first && i == 0 && c == 32) TRACE(14);
           }
         }
         release_acc();
@@ -599,10 +645,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                  __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3])));
             }
           }
+          if (lane == 0 && q == 0 && first) TRACE(7);  // partials stored
           release_acc();
           __threadfence();
           named_bar_sync(1, 128);
           if (q == 0 && lane == 0) red_release_gpu_add(&g.counters[region], 1);
+          if (lane == 0 && q == 0 && first) TRACE(8);  // published
         } else {
           if (q == 0 && lane == 0) {
             const int need = c_last - c_first;
@@ -611,68 +659,52 @@ __global__ void __launch_bounds__(kThreads, 1)
             g.counters[region] = 0;  // re-arm for the next launch / graph replay
           }
           named_bar_sync(1, 128);
+          if (lane == 0 && q == 0) TRACE(9);  // finisher: contributors in
           __threadfence();
+          // The first contributor's partial and the residual of a chunk are requested together,
+          // before the TMEM load, so the chunk costs one L2 round trip.
+          auto part_ptr = [&](int c2, int i, int c) {
+            return reinterpret_cast<const float4*>(g.ws + (((size_t)c2 * kPair + rank) * MT + i) * part_floats +
+                                                   ((size_t)c * 4 + q) * 1024) + lane;
+          };
           for (int i = 0; i < MT; ++i) {
             const int m0 = mbase + i * kBM * kPair;
+            if (m0 >= g.M_valid) continue;
             for (int c = 0; c < nchunk; ++c) {
+              float4 pf[8];
+              EpiPre pre;
+              {
+                const float4* s0 = part_ptr(c_first, i, c);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) pf[j] = __ldcg(s0 + j * 32);
+                epi_preload(g, lane, m0, nt * BN + c * 32, pre);
+              }
               uint32_t v[32];
               tmem_ld_sum(tbase + (uint32_t)(i * BN + c * 32), KA, sub_stride, v);
-              if (m0 >= g.M_valid) continue;
-              float acc_v[32];
-#pragma unroll
-              for (int j = 0; j < 32; ++j) acc_v[j] = __uint_as_float(v[j]);
-              int c2 = c_first;
-              for (; c2 + 1 < c_last; c2 += 2) {  // two contributors in flight
-                const float4* s0 = reinterpret_cast<const float4*>(
-                                       g.ws + (((size_t)c2 * kPair + rank) * MT + i) * part_floats +
-                                       ((size_t)c * 4 + q) * 1024) + lane;
-                const float4* s1 = reinterpret_cast<const float4*>(
-                                       g.ws + (((size_t)(c2 + 1) * kPair + rank) * MT + i) * part_floats +
-                                       ((size_t)c * 4 + q) * 1024) + lane;
-                float4 f0[8], f1[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) f0[j] = __ldcg(s0 + j * 32);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) f1[j] = __ldcg(s1 + j * 32);
+              auto add4 = [&](const float4 (&f)[8]) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                  acc_v[4 * j] += f0[j].x;
-                  acc_v[4 * j + 1] += f0[j].y;
-                  acc_v[4 * j + 2] += f0[j].z;
-                  acc_v[4 * j + 3] += f0[j].w;
+                  v[4 * j] = __float_as_uint(__uint_as_float(v[4 * j]) + f[j].x);
+                  v[4 * j + 1] = __float_as_uint(__uint_as_float(v[4 * j + 1]) + f[j].y);
+                  v[4 * j + 2] = __float_as_uint(__uint_as_float(v[4 * j + 2]) + f[j].z);
+                  v[4 * j + 3] = __float_as_uint(__uint_as_float(v[4 * j + 3]) + f[j].w);
                 }
+              };
+              add4(pf);
+              for (int c2 = c_first + 1; c2 < c_last; ++c2) {  // further contributors, in cluster order
+                const float4* s0 = part_ptr(c2, i, c);
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                  acc_v[4 * j] += f1[j].x;
-                  acc_v[4 * j + 1] += f1[j].y;
-                  acc_v[4 * j + 2] += f1[j].z;
-                  acc_v[4 * j + 3] += f1[j].w;
-                }
+                for (int j = 0; j < 8; ++j) pf[j] = __ldcg(s0 + j * 32);
+                add4(pf);
               }
-              if (c2 < c_last) {
-                const float4* s0 = reinterpret_cast<const float4*>(
-                                       g.ws + (((size_t)c2 * kPair + rank) * MT + i) * part_floats +
-                                       ((size_t)c * 4 + q) * 1024) + lane;
-                float4 f0[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) f0[j] = __ldcg(s0 + j * 32);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                  acc_v[4 * j] += f0[j].x;
-                  acc_v[4 * j + 1] += f0[j].y;
-                  acc_v[4 * j + 2] += f0[j].z;
-                  acc_v[4 * j + 3] += f0[j].w;
-                }
-              }
-#pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(acc_v[j]);
               if (nt * BN + c * 32 < g.N_valid) {
                 if (g.glu) epi_block_glu(g, stg, lane, m0, nt * BN + c * 32, v);
-                else epi_block(g, stg, lane, m0, nt * BN + c * 32, v);
+                else epi_block(g, stg, lane, m0, nt * BN + c * 32, v, pre);
               }
             }
           }
           release_acc();
+          if (lane == 0 && q == 0) TRACE(10);  // finisher: tile stored
         }
       }
       if (lane == 0 && q == 0 && first) TRACE(5);
@@ -694,8 +726,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ------------------------------------------------------------------ host side
 
 int gemm_set_trace(unsigned long long* buf) {
-  cudaError_t e = cudaMemcpyToSymbol(g_gemm_trace, &buf, sizeof(buf));
-  return e == cudaSuccess ? 0 : set_cuda_error("gemm trace", e);
+  g_trace_host = buf;
+  g_trace_launch = 0;
+  return 0;
 }
 
 static int gemm_smem_bytes(int a_bytes, int b_rows_per_cta, int stages) {
@@ -778,6 +811,7 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
   g.a_blocked = blocked;
   g.pf_dist = (variant & 4) ? 8 : 0;
   g.dbg = (pair == 1 && variant > 0) ? (variant >> 3) & 3 : 0;
+  if (variant > 0 && (variant & (1 << 12))) g.dbg |= 4;  // debug: epilogue skips its global stores
   int KA = 1;
   if (variant > 0 && ((variant >> 9) & 3)) KA = 1 << ((variant >> 9) & 3);
   while (KA > 1 && KA * MT * BN > 512) KA >>= 1;
@@ -814,6 +848,7 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
   g.residual = reinterpret_cast<const __nv_bfloat16*>(residual);
   g.bias = reinterpret_cast<const __nv_bfloat16*>(bias);
   if (rope) g.rp = *rope;
+  if (g_trace_host) g.trace = g_trace_host + (size_t)(g_trace_launch++ % 16) * 148 * 16;
   if (swap) {
     g.hint_a = kEvictFirst;  // weights stream once
     g.hint_b = kEvictLast;   // activations reused by every weight tile

@@ -17,7 +17,7 @@ for (T, O, K, mode, sms) in shapes:
     x = torch.randn(T, K, device=dev).bfloat16()
     w = (torch.randn(O, K, device=dev) * 0.02).bfloat16()
     y = torch.empty(T, O, device=dev, dtype=torch.bfloat16)
-    tr = torch.zeros(148 * 8, dtype=torch.int64, device=dev)
+    tr = torch.zeros(16 * 148 * 16, dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.int8, device=dev)
     for _ in range(3):
         ops.linear(x, w, out=y, mode=mode, num_sms=sms, scratch=sc)
@@ -31,13 +31,13 @@ for (T, O, K, mode, sms) in shapes:
     torch.cuda.synchronize()
     print(f"  event-timed launch: {ev0.elapsed_time(ev1) * 1e3:.2f} us")
     lib.rb_debug_gemm_trace(None)
-    t = tr.view(148, 8).cpu()
+    t = tr[: 148 * 16].view(148, 16).cpu()
     used = t[:, 0] > 0
     t = t[used]
     t0 = t[:, 0].min()
     rel = (t - t0).float() / 1000.0  # us
     print(f"T={T} O={O} K={K} mode={mode} sms={sms} ctas={int(used.sum())}")
-    names = ["start", "setup", "mma_first_full", "mma_last_full", "epi_tfull", "epi_done", "end"]
+    names = ["start", "setup", "mma_first_full", "mma_last_full", "epi_tfull", "epi_done", "end", "c_stored", "c_published", "f_in", "f_done"]
     for i, nm in enumerate(names):
         col = rel[:, i]
         ok = col[t[:, i] > 0] if i in (2, 3) else col
