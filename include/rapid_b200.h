@@ -154,6 +154,9 @@ typedef struct {
    * kernel); 1: q/k rows pair-interleaved within each head (row 2j = dim j, 2j+1 = dim
    * j+64), RoPE and the paged K/V write fused into the QKV GEMM epilogue. */
   int qk_layout;
+  /* tensor parallel: this rank's q/kv heads, intermediate and vocab above are its shard;
+   * global token id of local lm_head row v is vocab_offset + v (0 on a single GPU). */
+  int vocab_offset;
 } rb_model_t;
 
 typedef struct {
@@ -166,6 +169,7 @@ typedef struct {
   int gemm_counters_len;
   void* attn_ws;
   size_t attn_ws_bytes;
+  void* tp;  /* this phase's TP context from rb_tp_create (NULL: single GPU) */
 } rb_workspace_t;
 
 typedef struct {
@@ -180,6 +184,30 @@ typedef struct {
 } rb_batch_t;
 
 int rb_decoder_forward(const rb_model_t* model, const rb_workspace_t* ws, const rb_batch_t* batch, void* stream);
+
+/* Tensor parallelism (cfg 4, 70B TP=8). The reference models no
+ * collective (tp folds into GpuSpec.aggregate, pkg/src/pdsim/core.py:147-165); these
+ * realize the one all-reduce after each row-parallel GEMM (O, down) and the
+ * vocab-parallel greedy argmax. Each phase (prefill, decode) owns one context.
+ * mode 1: NCCL (dlopen'ed libnccl.so.2; comm from rb_tp_nccl_comm_init).
+ * mode 2: one-shot all-reduce over peer memory with the residual add fused: part0/part1
+ *   [world] = every rank's two staging buffers (part_elems bf16 each), flags[world] =
+ *   every rank's zeroed uint32 flag array (rb_tp_flag_words() words), epoch = this rank's
+ *   zeroed uint32 [128]; keys[world] = uint64 argmax key buffers (rows_cap each).
+ * Pointers are device pointers valid in this process (cudaIpc-opened on a multi-GPU
+ * node; plain pointers when ranks share one device). */
+int rb_tp_nccl_available(void);
+int rb_tp_nccl_unique_id(void* id_out /* 128 bytes */);
+int rb_tp_nccl_comm_init(const void* id /* 128 bytes */, int nranks, int rank, void** comm_out);
+int rb_tp_nccl_comm_destroy(void* comm);
+int rb_tp_create(int world, int rank, int mode, void* nccl_comm, void* const* part0, void* const* part1,
+                 void* const* keys, void* const* flags, void* epoch, size_t part_elems, void** tp_out);
+int rb_tp_destroy(void* tp);
+size_t rb_tp_flag_words(void);
+/* debug: skip the peer flag wait (results are then undefined) */
+int rb_tp_debug_nowait(void* tp, int on);
+/* standalone sum all-reduce of a bf16 vector (tests / benchmarks) */
+int rb_tp_allreduce(void* tp, void* x, long long n, void* stream);
 
 /* K7 — SM partitioning with CUDA green contexts (replaces the CU-fraction
  * scalars of AllocationDecision, pkg/src/pdsim/core.py:215-245, and the

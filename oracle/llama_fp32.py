@@ -141,6 +141,42 @@ class Oracle:
         logits = x @ s.get("lm_head", s["embed"]).T
         return logits, new_kv
 
+    def forward_tp(self, ids: torch.Tensor, shards: list[dict], la) -> torch.Tensor:
+        """The same prompt forward computed shard by shard (tensor parallel, test restatement
+        of paper_2601_11822_b200/tp.py): column-parallel QKV / gate|up, row-parallel O / down
+        whose partials are summed (the all-reduce), vocab-parallel lm_head concatenated.
+        shards[r] = tp.shard_state(...) of rank r, la = tp.local_arch(...). Returns [T, V]."""
+        a, s = self.a, self.s
+        T = ids.shape[0]
+        D = a.head_dim
+        G = la.q_heads // la.kv_heads
+        pos = torch.arange(T)
+        x = s["embed"][ids.long()]
+        for i in range(a.layers):
+            p = f"layers.{i}."
+            h = _rms(x, s[p + "ln1"], a.rms_eps)
+            attn_sum = torch.zeros_like(x)
+            for sh in shards:
+                q, k, v = h @ sh[p + "q"].T, h @ sh[p + "k"].T, h @ sh[p + "v"].T
+                if a.qkv_bias:
+                    q, k, v = q + sh[p + "bq"], k + sh[p + "bk"], v + sh[p + "bv"]
+                q = _rope(q.view(T, la.q_heads, D), pos, self.freqs)
+                k = _rope(k.view(T, la.kv_heads, D), pos, self.freqs)
+                v = v.view(T, la.kv_heads, D)
+                sc = torch.einsum("thd,nhd->htn", q, k.repeat_interleave(G, 1)) / math.sqrt(D)
+                sc = sc.masked_fill((pos[None, :] > pos[:, None])[None], float("-inf"))
+                o = torch.einsum("htn,nhd->thd", torch.softmax(sc, -1), v.repeat_interleave(G, 1))
+                attn_sum = attn_sum + o.reshape(T, -1) @ sh[p + "o"].T  # partial of the row-parallel O
+            x = x + attn_sum
+            h = _rms(x, s[p + "ln2"], a.rms_eps)
+            mlp_sum = torch.zeros_like(x)
+            for sh in shards:
+                mlp_sum = mlp_sum + (torch.nn.functional.silu(h @ sh[p + "gate"].T) * (h @ sh[p + "up"].T)) @ \
+                    sh[p + "down"].T
+            x = x + mlp_sum
+        x = _rms(x, s["norm"], a.rms_eps)
+        return torch.cat([x @ sh["lm_head"].T for sh in shards], dim=-1)
+
     def greedy(self, prompt: torch.Tensor, n_out: int):
         """Greedy continuation: returns (token ids [n_out], logits of each emitting step [n_out, V])."""
         logits, kv = self.forward(prompt, 0, None)

@@ -35,6 +35,11 @@ int embed_launch(const int* ids, const int* slot_of_row, const int* last_tok, co
                  int* ids_out, cudaStream_t st);
 int argmax_launch(const void* logits, long long ld, int T, int V, int* out, const int* slot_of_row, int* last_tok,
                   const int* row_valid, cudaStream_t st);
+void* tp_gemm_out(void* tp, void* x, const void** residual);
+void tp_begin(void* tp);
+int tp_reduce(void* tp, void* x, long long n, cudaStream_t st);
+int tp_argmax(void* tp, const void* logits, long long ld, int T, int V_local, int offset, int* out,
+              const int* slot_of_row, int* last_tok, const int* row_valid, cudaStream_t st);
 }  // namespace rb
 
 #define RB_TRY(x)          \
@@ -61,6 +66,8 @@ extern "C" int rb_decoder_forward(const rb_model_t* m, const rb_workspace_t* w, 
   char* attn = static_cast<char*>(w->attn);
   char* act = static_cast<char*>(w->act);
   const int sms = b->num_sms;
+  void* tp = w->tp;  // tensor-parallel context of this phase (NULL: single GPU)
+  tp_begin(tp);
   // ---- embedding: decode rows from device slot state, prefill rows from ids[]
   if (nd > 0) {
     if (b->ids_from_slots)
@@ -94,8 +101,13 @@ extern "C" int rb_decoder_forward(const rb_model_t* m, const rb_workspace_t* w, 
                                          m->block_table + (size_t)b->prefill_slot * m->bt_stride, np,
                                          b->prefill_start, Hq, Hkv, D, attn + (size_t)nd * Hq * D * e,
                                          (long long)Hq * D, m->attn_scale, m->num_blocks, st));
-    RB_TRY(gemm_bf16_launch(attn, m->wo[l], x, nullptr, x, T, H, Hq * D, Hq * D, Hq * D, H, 0, sms, w->gemm_ws,
-                            w->gemm_ws_bytes, w->gemm_counters, w->gemm_counters_len, st));
+    {  // row-parallel under TP: partial -> all-reduce with the residual add
+      const void* res = x;
+      void* y = tp_gemm_out(tp, x, &res);
+      RB_TRY(gemm_bf16_launch(attn, m->wo[l], y, nullptr, res, T, H, Hq * D, Hq * D, Hq * D, H, 0, sms, w->gemm_ws,
+                              w->gemm_ws_bytes, w->gemm_counters, w->gemm_counters_len, st));
+      RB_TRY(tp_reduce(tp, x, (long long)T * H, st));
+    }
     RB_TRY(rmsnorm_launch(x, H, m->ln2[l], h, H, T, H, m->rms_eps, st));
     // gate|up (rows interleaved in 16-blocks): token-major tiles fuse the SwiGLU into the
     // GEMM epilogue; swap-AB (decode) tiles measured faster with the separate kernel.
@@ -108,8 +120,13 @@ extern "C" int rb_decoder_forward(const rb_model_t* m, const rb_workspace_t* w, 
                               w->gemm_ws_bytes, w->gemm_counters, w->gemm_counters_len, st));
       RB_TRY(silu_mul_interleaved_launch(gu, 2 * I, act, I, T, I, st));
     }
-    RB_TRY(gemm_bf16_launch(act, m->wd[l], x, nullptr, x, T, H, I, I, I, H, 0, sms, w->gemm_ws, w->gemm_ws_bytes,
-                            w->gemm_counters, w->gemm_counters_len, st));
+    {
+      const void* res = x;
+      void* y = tp_gemm_out(tp, x, &res);
+      RB_TRY(gemm_bf16_launch(act, m->wd[l], y, nullptr, res, T, H, I, I, I, H, 0, sms, w->gemm_ws, w->gemm_ws_bytes,
+                              w->gemm_counters, w->gemm_counters_len, st));
+      RB_TRY(tp_reduce(tp, x, (long long)T * H, st));
+    }
   }
   // ---- sampling rows: decode rows, plus the chunk's last row when it finishes a prompt
   int nl = 0;
@@ -127,8 +144,12 @@ extern "C" int rb_decoder_forward(const rb_model_t* m, const rb_workspace_t* w, 
                             w->gemm_ws, w->gemm_ws_bytes, w->gemm_counters, w->gemm_counters_len, st));
     if (b->sample) {
       // row_valid = seq (padding rows have seq 0); the emitted prefill row uses the slot of row nd
-      RB_TRY(argmax_launch(w->logits, m->vocab, nl, m->vocab, w->out_ids, w->slot, m->last_tok,
-                           b->emit_prefill && np > 0 ? nullptr : w->seq, st));
+      const int* valid = b->emit_prefill && np > 0 ? nullptr : w->seq;
+      if (tp)  // vocab-parallel lm_head: max-reduce of (logit, -index) keys over the ranks
+        RB_TRY(tp_argmax(tp, w->logits, m->vocab, nl, m->vocab, m->vocab_offset, w->out_ids, w->slot, m->last_tok,
+                         valid, st));
+      else
+        RB_TRY(argmax_launch(w->logits, m->vocab, nl, m->vocab, w->out_ids, w->slot, m->last_tok, valid, st));
     }
   }
   return 0;

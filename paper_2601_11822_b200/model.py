@@ -99,8 +99,11 @@ class DecoderWeights:
         self.lm_head = lm_head
 
     @classmethod
-    def random(cls, arch: ArchConfig, device="cuda", seed: int = 0, std: float = 0.02) -> "DecoderWeights":
-        """Random-init weights of the real shapes (no checkpoints offline), generated on the device."""
+    def random(cls, arch: ArchConfig, device="cuda", seed: int = 0, std: float = 0.02,
+               embed_vocab: int | None = None) -> "DecoderWeights":
+        """Random-init weights of the real shapes (no checkpoints offline), generated on the device.
+        embed_vocab: rows of the (replicated) embedding when `arch` is a TP shard whose vocab
+        is the lm_head slice (tp.local_arch)."""
         g = torch.Generator(device=device).manual_seed(seed)
         H, D, I = arch.hidden, arch.head_dim, arch.intermediate
         nq = (arch.q_heads + 2 * arch.kv_heads) * D
@@ -116,7 +119,7 @@ class DecoderWeights:
             # random rows: already "pair-interleaved" (any permutation of random rows is random)
             layers.append(LayerWeights(n(H), w(nq, H), w(nq) if arch.qkv_bias else None, w(H, arch.q_heads * D), n(H),
                                        w(2 * I, H), w(H, I)))
-        embed = w(arch.vocab, H)
+        embed = w(embed_vocab or arch.vocab, H)
         lm = embed if arch.tie_embeddings else w(arch.vocab, H)
         return cls(arch, embed, layers, n(H), lm)
 
@@ -172,6 +175,7 @@ class _Buffers:
         self.slot = torch.zeros(rows, dtype=torch.int32, device=device)
         self.seq = torch.zeros(rows, dtype=torch.int32, device=device)
         self.out_ids = torch.zeros(rows, dtype=torch.int32, device=device)
+        self.tp = None  # tp.TpContext of this phase under tensor parallelism
         # split-K partials + tile counters of this phase's GEMMs (never shared across streams)
         self.scratch = ops.GemmScratch(device, ws_bytes=64 << 20, n_counters=8192)
 
@@ -181,7 +185,7 @@ class Runner:
 
     def __init__(self, weights: DecoderWeights, num_blocks: int, num_slots: int, max_blocks_per_seq: int,
                  max_prefill_tokens: int = 2048, max_decode_batch: int = 256, device="cuda",
-                 max_position: int | None = None):
+                 max_position: int | None = None, vocab_offset: int = 0):
         arch = weights.arch
         self.arch = arch
         self.w = weights
@@ -199,6 +203,7 @@ class Runner:
         self.cos_sin = rope_table(arch, mp).to(self.device)
         self.pre = _Buffers(arch, max_prefill_tokens, self.device, max_decode_batch + 1)
         self.dec = _Buffers(arch, max_decode_batch, self.device, max_decode_batch)
+        self.vocab_offset = vocab_offset  # TP rank's first lm_head row (global token id)
         self.max_prefill_tokens = max_prefill_tokens
         self.max_decode_batch = max_decode_batch
         self.scale = 1.0 / math.sqrt(arch.head_dim)
@@ -232,7 +237,8 @@ class Runner:
                             kv_cache=self.kv.data_ptr(), kv_layer_stride_bytes=self.kv[0].numel() * 2,
                             num_blocks=self.num_blocks, block_table=self.block_table.data_ptr(),
                             bt_stride=self.block_table.stride(0), cos_sin=self.cos_sin.data_ptr(),
-                            last_tok=self.last_tok.data_ptr(), qk_layout=1 if a.head_dim == 128 else 0)
+                            last_tok=self.last_tok.data_ptr(), qk_layout=1 if a.head_dim == 128 else 0,
+                            vocab_offset=self.vocab_offset)
             for k, v in keep.items():
                 setattr(m, k, ctypes.cast(v, ctypes.POINTER(ctypes.c_void_p)))
             self._mc = m
@@ -248,7 +254,7 @@ class Runner:
                                gemm_ws=B.scratch.ws.data_ptr(), gemm_ws_bytes=B.scratch.ws_bytes,
                                gemm_counters=B.scratch.counters.data_ptr(),
                                gemm_counters_len=B.scratch.counters.numel(), attn_ws=self.attn_ws.data_ptr(),
-                               attn_ws_bytes=self.attn_ws.numel() * 4)
+                               attn_ws_bytes=self.attn_ws.numel() * 4, tp=B.tp.handle if B.tp is not None else None)
 
     def kernels_per_forward(self, n_decode: int, n_prefill: int, logits_decode: bool, emit_prefill: bool,
                             sample: bool) -> int:

@@ -71,6 +71,16 @@ _SIGS = {
         _c_int,
     ),
     "rb_green_destroy": ([_vp], _c_int),
+    "rb_tp_nccl_available": ([], _c_int),
+    "rb_tp_nccl_unique_id": ([_vp], _c_int),
+    "rb_tp_nccl_comm_init": ([_vp, _c_int, _c_int, ctypes.POINTER(_vp)], _c_int),
+    "rb_tp_nccl_comm_destroy": ([_vp], _c_int),
+    "rb_tp_create": ([_c_int, _c_int, _c_int, _vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                      ctypes.POINTER(_vp), _vp, _c_size, ctypes.POINTER(_vp)], _c_int),
+    "rb_tp_destroy": ([_vp], _c_int),
+    "rb_tp_flag_words": ([], _c_size),
+    "rb_tp_debug_nowait": ([_vp, _c_int], _c_int),
+    "rb_tp_allreduce": ([_vp, _vp, _c_ll, _vp], _c_int),
 }
 
 class RbModel(ctypes.Structure):
@@ -83,14 +93,14 @@ class RbModel(ctypes.Structure):
         ("wo", ctypes.POINTER(_vp)), ("ln2", ctypes.POINTER(_vp)), ("wgu", ctypes.POINTER(_vp)),
         ("wd", ctypes.POINTER(_vp)), ("kv_cache", _vp), ("kv_layer_stride_bytes", _c_size), ("num_blocks", _c_int),
         ("block_table", _vp), ("bt_stride", _c_int), ("cos_sin", _vp), ("last_tok", _vp),
-        ("qk_layout", _c_int)]
+        ("qk_layout", _c_int), ("vocab_offset", _c_int)]
 
 
 class RbWorkspace(ctypes.Structure):
     _fields_ = [(n, _vp) for n in ("x", "h", "qkv", "q", "attn", "gu", "act", "logits")] + [("rows_cap", _c_int)] + [
         (n, _vp) for n in ("ids", "pos", "slot", "seq", "out_ids")] + [
         ("gemm_ws", _vp), ("gemm_ws_bytes", _c_size), ("gemm_counters", _vp), ("gemm_counters_len", _c_int),
-        ("attn_ws", _vp), ("attn_ws_bytes", _c_size)]
+        ("attn_ws", _vp), ("attn_ws_bytes", _c_size), ("tp", _vp)]
 
 
 class RbBatch(ctypes.Structure):
