@@ -172,7 +172,7 @@ def time_decode_attention(runner, stream, B: int, ctx: int, sms: int, iters: int
 
 
 def main():
-    global PROMPT, OUTPUT
+    global PROMPT, OUTPUT, SLO_ITL_US
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=600)
@@ -189,14 +189,16 @@ def main():
     ap.add_argument("--ref-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--engine", default="rapid", help="rapid | hybrid-<chunk> (same-engine chunked-prefill comparator)")
+    ap.add_argument("--slo-ms", type=float, default=SLO_ITL_US / 1e3, help="p99 ITL SLO (default 50 ms)")
     ap.add_argument("--arm-profile", default=None,
                     help="measured B200 ARM tables (profiler.py JSON); implies --arm with arm.MeasuredArm")
-    ap.add_argument("--arm-policy", default="balanced", choices=["balanced", "slo-min"])
+    ap.add_argument("--arm-policy", default="balanced", choices=["balanced", "slo-min", "adaptive"])
     ap.add_argument("--arm", action="store_true",
                     help="cfg 3: adaptive ARM (allocate() per launch) instead of the cfg-2 static split")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     PROMPT, OUTPUT = args.prompt, args.output
+    SLO_ITL_US = int(args.slo_ms * 1e3)
     if args.arm_profile:
         args.arm = True
 
@@ -336,6 +338,15 @@ def main():
     mctx = int(round(statistics.mean(win["ctxs"]))) if win["ctxs"] else PROMPT + OUTPUT // 2
     probe = time_decode_attention(ex.runner, part.ds, mB, mctx, part.d_sms)
     hbm = peaks["hbm_gbs"]
+    # DRAM traffic of the dominant kernel from the committed ncu --set full capture, per launch:
+    # measured bytes / algorithmic bytes at the capture shape, times this probe's algorithmic bytes
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            nt = json.load(fh)["decode_attn_tc_kernel"]
+        traffic = (nt["dram_bytes_read"] + nt["dram_bytes_write"]) / nt["algorithmic_bytes"] * probe["bytes"]
+    except (OSError, KeyError, ValueError):
+        pass
     steps = max(1, win["steps"])
     h2d = (win["h2d1"] - win["h2d0"]) / steps if complete else 0
     d2h = (win["d2h1"] - win["d2h0"]) / steps if complete else 0
@@ -405,7 +416,9 @@ def main():
                 "note": "host wall clock over the same K steps through RapidEngine/B200Executor (pinned H2D of "
                         "step inputs + block-table deltas + prefill ids, D2H of sampled ids, every step)"},
         "roofline": {"kernel": "decode_attn_tc_kernel (K3)", "bound": "hbm", "achieved": probe["gbs"], "peak": hbm,
-                     "unit": "GB/s", "frac": probe["gbs"] / hbm, "traffic": None,
+                     "unit": "GB/s", "frac": probe["gbs"] / hbm, "traffic": traffic,
+                     "traffic_src": "profiles/ncu_traffic.json (dram read+write / algorithmic bytes of one "
+                                    "ncu --set full launch, scaled to this probe)",
                      "per_launch": f"B={probe['B']} ctx={probe['ctx']}: {probe['bytes']} B (K+V bf16, 1 layer) "
                                    f"in {probe['ms'] * 1e3:.1f} us on the {d_sms}-SM decode partition",
                      "peak_src": peaks["_src"]},

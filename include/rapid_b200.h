@@ -38,9 +38,14 @@ int rb_debug_gemm_pair_mode(int mode);
 /* Debug: decode (swap-AB) GEMM schedule, -1 auto (default); else bit0 = two 128-row weight
  * sub-tiles per activation stage, bit1 = stream-K (else data-parallel whole tiles). */
 int rb_debug_gemm_variant(int v);
+/* Debug: stream-K for token-major (prefill) GEMMs whose whole-tile waves quantize badly
+ * (fewer than 4 waves, last wave at most max_frac full); default off (measured slower). */
+int rb_debug_gemm_prefill_streamk(int on, double max_frac);
 /* Programmatic dependent launch for the forward's kernels (default on): each kernel may
  * start its prologue while its predecessor in the stream drains. 0 = plain serialization. */
 int rb_set_pdl(int on);
+/* Decode (swap-AB) gate|up GEMM: 1 = SwiGLU fused into its epilogue, 0 = separate kernel. */
+int rb_set_decode_glu(int on);
 
 /* K1/K4 — bf16 linear layer on tcgen05 tensor cores:
  *   Y[t,o] = sum_k X[t,k] W[o,k] (+bias[o]) (+R[t,o])

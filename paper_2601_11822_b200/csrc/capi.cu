@@ -30,6 +30,7 @@ int prefill_attention_tc_launch(const void* q, long long q_tok_stride, const voi
 int gemm_set_trace(unsigned long long* buf);
 int gemm_set_pair_mode(int mode);
 int gemm_set_variant(int v);
+int gemm_set_prefill_streamk(int on, double max_frac);
 }  // namespace rb
 
 #define ST(s) reinterpret_cast<cudaStream_t>(s)
@@ -42,6 +43,7 @@ const char* rb_last_error(void) { return rb::last_error(); }
 int rb_debug_gemm_trace(unsigned long long* buf) { return rb::gemm_set_trace(buf); }
 int rb_debug_gemm_pair_mode(int mode) { return rb::gemm_set_pair_mode(mode); }
 int rb_debug_gemm_variant(int v) { return rb::gemm_set_variant(v); }
+int rb_debug_gemm_prefill_streamk(int on, double max_frac) { return rb::gemm_set_prefill_streamk(on, max_frac); }
 int rb_set_pdl(int on) {
   rb::set_pdl(on != 0);
   return 0;

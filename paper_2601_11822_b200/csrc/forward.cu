@@ -42,6 +42,13 @@ int tp_argmax(void* tp, const void* logits, long long ld, int T, int V_local, in
               const int* slot_of_row, int* last_tok, const int* row_valid, cudaStream_t st);
 }  // namespace rb
 
+// swap-AB (decode) gate|up: 1 = SwiGLU fused into the GEMM epilogue, 0 = separate kernel
+static int g_decode_glu = 0;
+extern "C" int rb_set_decode_glu(int on) {
+  g_decode_glu = on;
+  return 0;
+}
+
 #define RB_TRY(x)          \
   do {                     \
     int _rc = (x);         \
@@ -111,7 +118,7 @@ extern "C" int rb_decoder_forward(const rb_model_t* m, const rb_workspace_t* w, 
     RB_TRY(rmsnorm_launch(x, H, m->ln2[l], h, H, T, H, m->rms_eps, st));
     // gate|up (rows interleaved in 16-blocks): token-major tiles fuse the SwiGLU into the
     // GEMM epilogue; swap-AB (decode) tiles measured faster with the separate kernel.
-    if (T > 256) {
+    if (T > 256 || g_decode_glu) {
       RB_TRY(gemm_bf16_launch(h, m->wgu[l], act, nullptr, nullptr, T, 2 * I, H, H, H, I, 4, sms, w->gemm_ws,
                               w->gemm_ws_bytes, w->gemm_counters, w->gemm_counters_len, st));
     } else {

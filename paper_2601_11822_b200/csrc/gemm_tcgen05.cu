@@ -37,7 +37,12 @@ namespace rb {
 constexpr int kBM = 128;                // rows of A per CTA
 constexpr int kBK = 64;                 // bf16 elements per 128-byte swizzle row
 constexpr int kABytes = kBM * kBK * 2;  // 16 KB
-constexpr int kThreads = 192;
+// Epilogue warp sets (template kSets): each TMEM quadrant is drained by kSets warps taking
+// alternate 32-column chunks. Decode (swap-AB) GEMMs are short and their split-tile epilogue
+// is on the critical path: 2 sets (320 threads, 168 registers); prefill GEMMs overlap the
+// epilogue with the next tile's MMAs: 1 set (192 threads, no register cap).
+constexpr int threads_for(int sets) { return 64 + 128 * sets; }
+constexpr int kMaxEpiWarps = 8;
 constexpr int kStgStride = 40;          // bf16 per staging row (32 + 8 pad, 80 B)
 constexpr int kStgBytes = 32 * kStgStride * 2;  // per epilogue warp
 
@@ -386,10 +391,12 @@ __device__ __forceinline__ void tmem_ld_sum(uint32_t taddr, int ka, uint32_t str
   }
 }
 
-template <int kPair, int kMT>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int kPair, int kMT, int kSets>
+__global__ void __launch_bounds__(threads_for(kSets), 1)
     gemm_bf16_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
                              const __grid_constant__ CUtensorMap tmap_b, const GemmArgs g) {
+  constexpr int kEpiSets = kSets;
+  constexpr int kEpiWarps = 4 * kSets;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment by pointer arithmetic on the __shared__ array (an integer round
   // trip would drop the address space: every staging access would compile to generic LD/ST)
@@ -403,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + (size_t)stages * a_bytes;
   __nv_bfloat16* stg_all = reinterpret_cast<__nv_bfloat16*>(sB + (size_t)stages * b_bytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stg_all) + 4 * kStgBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stg_all) + kEpiWarps * kStgBytes);
   uint64_t* empty = full + stages;
   uint64_t* tfull = empty + stages;  // 2
   uint64_t* tempty = tfull + 2;      // 2
@@ -433,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4 * kPair);  // one arrive per epilogue warp of every CTA of the pair
+      mbar_init(&tempty[a], kEpiWarps * kPair);  // one arrive per epilogue warp of every CTA of the pair
     }
     fence_barrier_init();
   }
@@ -576,9 +583,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ================= epilogue warps 2..5 (both CTAs) =================
-    const int q = warp & 3;  // TMEM lane quadrant accessible by this warp
-    __nv_bfloat16* stg = stg_all + (size_t)q * (kStgBytes / 2);
+    // ================= epilogue warps 2.. (both CTAs) =================
+    // warp w may only read TMEM lane quadrant w % 4; the kEpiSets warps of a quadrant take
+    // alternate 32-column chunks of every accumulator (the epilogue is latency-bound per warp)
+    const int q = warp & 3;
+    const int ew = warp - 2;
+    const int set = ew >> 2;
+    const bool lead = lane == 0 && q == 0 && set == 0;  // one thread of the CTA's epilogue
+    __nv_bfloat16* stg = stg_all + (size_t)ew * (kStgBytes / 2);
     const uint32_t tempty_leader0 = (kPair == 2) ? mapa_shared(&tempty[0], 0) : 0u;
     const int nchunk = BN / 32;
     const size_t part_floats = (size_t)kBM * BN;  // one CTA's partial of one sub-tile
@@ -592,7 +604,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nt = t / g.m_tiles;
       const int mbase = mtile * tile_rows + (int)rank * kBM + q * 32;  // + i * kBM * kPair per sub-tile
       mbar_wait(&tfull[acc], acc_phase);
-      if (lane == 0 && q == 0 && first) TRACE(4);
+      if (lead && first) TRACE(4);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)acc * acc_stride;
       auto release_acc = [&]() {
@@ -608,18 +620,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < MT; ++i) {
           const int m0 = mbase + i * kBM * kPair;
           if (m0 >= g.M_valid) continue;
-          for (int c = 0; c < BN; c += 32) {
+          for (int c = set * 32; c < BN; c += 32 * kEpiSets) {
             EpiPre pre;
             epi_preload(g, lane, m0, nt * BN + c, pre);
             uint32_t v[32];
-            if (lane == 0 && q == 0 && first && i == 0 && c < 64) TRACE(11 + (c >> 5));
+            if (lead && first && i == 0 && c < 64) TRACE(11 + (c >> 5));
             tmem_ld_sum(tbase + (uint32_t)(i * BN + c), KA, sub_stride, v);
-            if (lane == 0 && q == 0 && first && i == 0 && c == 32) TRACE(13);
+            if (lead && first && i == 0 && c == 32) TRACE(13);
             if (nt * BN + c < g.N_valid) {
               if (g.glu) epi_block_glu(g, stg, lane, m0, nt * BN + c, v);
-              else epi_block(g, stg, lane, m0, nt * BN + c, v, pre, lane == 0 && q == 0 && first && i == 0 && c == 32);
+              else epi_block(g, stg, lane, m0, nt * BN + c, v, pre, lead && first && i == 0 && c == 32);
             }
-            if (lane == 0 && q == 0 && first && i == 0 && c == 32) TRACE(14);
+            if (lead && first && i == 0 && c == 32) TRACE(14);
           }
         }
         release_acc();
@@ -634,7 +646,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (cid != c_last) {
           float* mine = g.ws + (((size_t)cid * kPair + rank) * MT) * part_floats;
           for (int i = 0; i < MT; ++i) {
-            for (int c = 0; c < nchunk; ++c) {
+            for (int c = set; c < nchunk; c += kEpiSets) {
               uint32_t v[32];
               tmem_ld_sum(tbase + (uint32_t)(i * BN + c * 32), KA, sub_stride, v);
               // lane-major layout: float4 j of lane l at (j*32 + l) -> 512 contiguous bytes per store
@@ -645,21 +657,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                  __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3])));
             }
           }
-          if (lane == 0 && q == 0 && first) TRACE(7);  // partials stored
+          if (lead && first) TRACE(7);  // partials stored
           release_acc();
           __threadfence();
-          named_bar_sync(1, 128);
-          if (q == 0 && lane == 0) red_release_gpu_add(&g.counters[region], 1);
-          if (lane == 0 && q == 0 && first) TRACE(8);  // published
+          named_bar_sync(1, 32 * kEpiWarps);
+          if (lead) red_release_gpu_add(&g.counters[region], 1);
+          if (lead && first) TRACE(8);  // published
         } else {
-          if (q == 0 && lane == 0) {
+          if (lead) {
             const int need = c_last - c_first;
             while (ld_acquire_gpu(&g.counters[region]) < need) {
             }
             g.counters[region] = 0;  // re-arm for the next launch / graph replay
           }
-          named_bar_sync(1, 128);
-          if (lane == 0 && q == 0) TRACE(9);  // finisher: contributors in
+          named_bar_sync(1, 32 * kEpiWarps);
+          if (lead) TRACE(9);  // finisher: contributors in
           __threadfence();
           // The first contributor's partial and the residual of a chunk are requested together,
           // before the TMEM load, so the chunk costs one L2 round trip.
@@ -670,7 +682,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int i = 0; i < MT; ++i) {
             const int m0 = mbase + i * kBM * kPair;
             if (m0 >= g.M_valid) continue;
-            for (int c = 0; c < nchunk; ++c) {
+            for (int c = set; c < nchunk; c += kEpiSets) {
               float4 pf[8];
               EpiPre pre;
               {
@@ -704,10 +716,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           release_acc();
-          if (lane == 0 && q == 0) TRACE(10);  // finisher: tile stored
+          if (lead) TRACE(10);  // finisher: tile stored
         }
       }
-      if (lane == 0 && q == 0 && first) TRACE(5);
+      if (lead && first) TRACE(5);
       if (++acc == g.nacc) { acc = 0; acc_phase ^= 1; }
       first = false;
     }
@@ -732,7 +744,8 @@ int gemm_set_trace(unsigned long long* buf) {
 }
 
 static int gemm_smem_bytes(int a_bytes, int b_rows_per_cta, int stages) {
-  return stages * (a_bytes + b_rows_per_cta * kBK * 2) + 4 * kStgBytes + 1024 /*align*/ + (2 * stages + 4) * 8 + 32;
+  return stages * (a_bytes + b_rows_per_cta * kBK * 2) + kMaxEpiWarps * kStgBytes + 1024 /*align*/ +
+         (2 * stages + 4) * 8 + 32;
 }
 
 static int g_force_pair = -1;  // debug override: -1 auto, 0 single-CTA, 1 CTA pair
@@ -743,6 +756,13 @@ int gemm_set_pair_mode(int mode) {
 // debug override of the decode (swap-AB) schedule: -1 auto; else bit0 = 2 A sub-tiles
 // per tile, bit1 = stream-K (without it: data-parallel whole tiles)
 static int g_force_variant = -1;
+static int g_prefill_streamk = 0;          // stream-K for badly wave-quantized token-major GEMMs
+static double g_prefill_streamk_frac = 0.6;
+int gemm_set_prefill_streamk(int on, double max_frac) {
+  g_prefill_streamk = on;
+  g_prefill_streamk_frac = max_frac;
+  return 0;
+}
 int gemm_set_variant(int v) {
   g_force_variant = v;
   return 0;
@@ -801,7 +821,7 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
   const int bn_cta = BN / pair;
   const int a_bytes = MT * kABytes;
   const int stage_bytes = a_bytes + bn_cta * kBK * 2;
-  int stages = (200 * 1024 - 4 * kStgBytes) / stage_bytes;
+  int stages = (200 * 1024 - kMaxEpiWarps * kStgBytes) / stage_bytes;
   if (stages > 8) stages = 8;
   if (stages < 2) stages = 2;
   if (variant > 0 && ((variant >> 5) & 15) >= 2 && ((variant >> 5) & 15) <= stages) stages = (variant >> 5) & 15;
@@ -825,6 +845,15 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
   const int slots = num_sms / pair;  // concurrent clusters
   int clusters = g.total_tiles < slots ? g.total_tiles : slots;
   g.streamk = 0;
+  if (!swap && g_force_variant < 0 && g_prefill_streamk) {
+    // token-major (prefill) tiles (off by default: measured slower, the split-tile fixup costs
+    // more than the quantization it removes): stream-K only where whole-tile waves quantize badly
+    // (a few waves with a small last one, e.g. the O / down projections of a 1K-token
+    // chunk: 64 tiles on 42 clusters = 1.5 waves run as 2); long GEMMs stay data-parallel
+    const double waves = (double)g.total_tiles / slots;
+    const double frac = waves - (int)waves;
+    if (waves < 4.0 && frac > 0.0 && frac <= g_prefill_streamk_frac) variant |= 2;
+  }
   if ((variant & 2) && workspace != nullptr && counters != nullptr && g.total_tiles * pair <= counters_len &&
       g.total_tiles % slots != 0) {
     // every cluster gets >= 8 k-blocks; one partial slot per cluster: [cluster][pair][MT][128 x BN] fp32
@@ -870,16 +899,21 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
 
   const int smem = gemm_smem_bytes(a_bytes, bn_cta, stages);
   using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const GemmArgs);
-  static const KernelFn kernels[2][2] = {{gemm_bf16_tcgen05_kernel<1, 1>, gemm_bf16_tcgen05_kernel<1, 2>},
-                                         {gemm_bf16_tcgen05_kernel<2, 1>, gemm_bf16_tcgen05_kernel<2, 2>}};
-  static bool attr_done[2][2] = {{false, false}, {false, false}};
-  const KernelFn kern = kernels[pair - 1][MT - 1];
-  if (!attr_done[pair - 1][MT - 1]) {
+  // [pair][MT][sets]: decode (swap-AB) with single A sub-tiles uses 2 epilogue sets
+  static const KernelFn kernels[2][2][2] = {
+      {{gemm_bf16_tcgen05_kernel<1, 1, 1>, gemm_bf16_tcgen05_kernel<1, 1, 2>},
+       {gemm_bf16_tcgen05_kernel<1, 2, 1>, gemm_bf16_tcgen05_kernel<1, 2, 1>}},
+      {{gemm_bf16_tcgen05_kernel<2, 1, 1>, gemm_bf16_tcgen05_kernel<2, 1, 2>},
+       {gemm_bf16_tcgen05_kernel<2, 2, 1>, gemm_bf16_tcgen05_kernel<2, 2, 1>}}};
+  static bool attr_done[2][2][2] = {};
+  const int sets = (swap && MT == 1) ? 2 : 1;
+  const KernelFn kern = kernels[pair - 1][MT - 1][sets - 1];
+  if (!attr_done[pair - 1][MT - 1][sets - 1]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return set_cuda_error("gemm: set smem attr", e);
-    attr_done[pair - 1][MT - 1] = true;
+    attr_done[pair - 1][MT - 1][sets - 1] = true;
   }
-  cudaError_t e = launch_k(kern, dim3(pair * clusters), dim3(kThreads), smem, stream, pair, ta, tb, g);
+  cudaError_t e = launch_k(kern, dim3(pair * clusters), dim3(threads_for(sets)), smem, stream, pair, ta, tb, g);
   if (e != cudaSuccess) return set_cuda_error("gemm launch", e);
   return 0;
 }

@@ -313,6 +313,19 @@ __device__ __forceinline__ void tma_prefetch_l2_2d_w(const void* tmap, int32_t x
 
 // ---------------------------------------------------------------- PDL
 // Let the next kernel in the stream launch (its CTAs park in pdl_wait until we finish).
+// 1D bulk copy global -> this CTA's smem, completion counted on `bar` (bytes % 16 == 0)
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst_smem)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+// 16-byte async copy global -> smem (L2 only), completed by cp_async_wait_all
+__device__ __forceinline__ void cp_async_16(void* dst_smem, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 // Block until the preceding kernel has completed and its writes are visible (no-op
 // when this kernel was not launched with programmatic stream serialization).

@@ -31,7 +31,9 @@ _SIGS = {
     "rb_debug_gemm_trace": ([_vp], _c_int),
     "rb_debug_gemm_pair_mode": ([_c_int], _c_int),
     "rb_debug_gemm_variant": ([_c_int], _c_int),
+    "rb_debug_gemm_prefill_streamk": ([_c_int, ctypes.c_double], _c_int),
     "rb_set_pdl": ([_c_int], _c_int),
+    "rb_set_decode_glu": ([_c_int], _c_int),
     "rb_gemm_bf16": (
         [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_ll, _c_ll, _c_ll, _c_int, _c_int, _vp, _c_size, _vp,
          _c_int, _vp],

@@ -13,7 +13,8 @@ latency against prefill throughput.
     python -m paper_2601_11822_b200.profiler --model llama3.1-8b --ctx 1152 --out profiles/arm_llama8b.json
 
 The JSON holds {"decode_us": {D: {B: us}}, "overalloc_decode_us": {B: us},
-"prefill_us_per_token": {D: us}, ...}; `MeasuredProfile` (arm.py) reads it and
+"prefill_us_per_token": {D: us}, "prefill_us_per_token_by_batch": {D: {B: us}}, ...};
+`MeasuredProfile` (arm.py) reads it and
 writes the reference's interchange lines `batch,fraction[,saturated]`.
 """
 
@@ -84,7 +85,7 @@ def measure(model: str = "llama3.1-8b", ctx: int = 1152, chunk: int = 2048, ladd
             ps.synchronize()
             pts.append(a.elapsed_time(b) * 1e3)
         p_alone = _med(pts)
-        dec, pre_conc = {}, []
+        dec, pre_conc, pre_by_b = {}, [], {}
         for B in batches:
             with torch.cuda.stream(ds):
                 r.decode_body(B, num_sms=d_sms, max_pages=mp, stream=ds.cuda_stream)
@@ -116,23 +117,26 @@ def measure(model: str = "llama3.1-8b", ctx: int = 1152, chunk: int = 2048, ladd
                 dts.append(e0.elapsed_time(e1) * 1e3 / steps)
                 pre_conc.append(a.elapsed_time(b) * 1e3 / min(n_chunks, 16))
             dec[B] = round(_med(dts), 1)
+            pre_by_b[B] = round(_med(pre_conc[-reps:]) / chunk, 3)
             del g
-        return dec, _med(pre_conc) / chunk, p_alone / chunk
+        return dec, _med(pre_conc) / chunk, p_alone / chunk, pre_by_b
 
     for D in ladder:
         t0 = time.perf_counter()
         gs = ops.GreenSplit(D)
         ds, ps = gs.streams
-        dec, p_tok, p_alone_tok = run_partition(ds, ps, gs.sms[0], gs.sms[1])
+        dec, p_tok, p_alone_tok, p_by_b = run_partition(ds, ps, gs.sms[0], gs.sms[1])
         out["decode_us"][str(gs.sms[0])] = dec
+        out.setdefault("prefill_us_per_token_by_batch", {})[str(gs.sms[0])] = p_by_b
         out["prefill_us_per_token"][str(gs.sms[0])] = round(p_tok, 3)
         out["prefill_alone_us_per_token"][str(gs.sms[0])] = round(p_alone_tok, 3)
         log(f"decode {gs.sms[0]:3d} SMs / prefill {gs.sms[1]:3d}: prefill {p_tok:.2f} us/token under load "
             f"({p_alone_tok:.2f} alone); decode us {dec}  [{time.perf_counter() - t0:.1f} s]")
     # OVERALLOCATE: both phases on the whole device, two ordinary streams
     ds, ps = torch.cuda.Stream(), torch.cuda.Stream()
-    dec, p_tok, p_alone_tok = run_partition(ds, ps, total, total)
+    dec, p_tok, p_alone_tok, p_by_b = run_partition(ds, ps, total, total)
     out["overalloc_decode_us"] = dec
+    out.setdefault("prefill_us_per_token_by_batch", {})["overalloc"] = p_by_b
     out["overalloc_prefill_us_per_token"] = round(p_tok, 3)
     out["full_prefill_alone_us_per_token"] = round(p_alone_tok, 3)
     log(f"overallocate: prefill {p_tok:.2f} us/token under load ({p_alone_tok:.2f} alone); decode us {dec}")

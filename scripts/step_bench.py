@@ -63,6 +63,7 @@ def main():
     out = []
     for pdl in [int(x) for x in args.pdl.split(",")]:
         lib.rb_set_pdl(pdl)
+        lib.rb_set_decode_glu(int(os.environ.get("RB_DECODE_GLU", "0")))
         for B in Bs:
             with torch.cuda.stream(ds):
                 r.decode_body(B, num_sms=gs.sms[0], max_pages=mp, stream=ds.cuda_stream)

@@ -86,3 +86,25 @@ def test_splits_used_covers_decisions():
 def test_bad_policy():
     with pytest.raises(ValueError):
         MeasuredArm(MeasuredProfile(synth()), 50_000, policy="nope")
+
+
+def test_adaptive_policy_walks_with_queue_feedback():
+    mp = MeasuredProfile(synth())
+    arm = MeasuredArm(mp, 50_000, max_batch=256, policy="adaptive")
+    d0 = decode_sms_of(arm.decide(128, 2048, 0.25), 148)
+    assert d0 == arm._balanced(128, 0.25)
+    # decode-bound windows (decoders waiting beyond max_batch) move decode up one granule
+    for _ in range(arm.WINDOW):
+        arm.observe(20_000, 256, 5, 3)
+    d1 = decode_sms_of(arm.decide(256, 2048, 0.25), 148)
+    assert d1 is not None and d1 > d0
+    # a standing prefill queue with decode slack moves one granule back
+    for _ in range(arm.WINDOW):
+        arm.observe(15_000, 128, 0, 4)
+    d2 = decode_sms_of(arm.decide(128, 2048, 0.25), 148)
+    assert d2 < d1
+    # every split the walk can reach is pre-captured
+    i = mp.ladder.index(d0)
+    assert set(mp.ladder[max(0, i - arm.SPAN):i + arm.SPAN + 1]) <= arm.splits_used()
+    # idle phases still overallocate
+    assert arm.decide(0, 100, 0.25).mode is AllocationMode.OVERALLOCATE
