@@ -1,15 +1,19 @@
 """Headline benchmark: RAPID-Serve on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--qps Q] [--duration S] [--decode-sms 72] [--model llama3.1-8b]
+                    [--qps Q] [--duration S] [--model llama3.1-8b] [--slo-ms 50]
+                    [--decode-sms 72 | --arm | --arm-profile PATH --arm-policy adaptive|balanced|slo-min]
+                    [--engine rapid|hybrid-<chunk>] [--prompt 1024 --output 256]
 
-Workload (BASELINE.json configs[1], "cfg 2"): Llama-3.1-8B bf16 (random-init
-weights of the real shapes; no checkpoints offline), one B200, static SM split
-(decode 72 SMs = 9x8, prefill 76 SMs: the green-context-granular 50/50),
-synthetic trace `synthesize(WorkloadSpec(qps=Q, duration_s=S, seed=42,
-mean_prompt_tokens=1024, mean_output_tokens=256, sigma=0))` served by the
-real-time RAPID engine (prefill and decode of different requests concurrently
-on disjoint SM partitions over one shared paged KV cache).
+Workload (BASELINE.json configs[2], "cfg 3", the configuration the SLO-constrained metric
+is defined on): Llama-3.1-8B bf16 (random-init weights of the real shapes; no checkpoints
+offline), one B200, synthetic trace `synthesize(WorkloadSpec(qps=Q, duration_s=S, seed=42,
+mean_prompt_tokens=1024, mean_output_tokens=256, sigma=0))` served by the real-time RAPID
+engine (prefill and decode of different requests concurrently on disjoint SM partitions
+over one shared paged KV cache) with the measured adaptive ARM (profiles/arm/)
+choosing the green-context split at every launch. `--decode-sms 72` runs cfg 2 (static
+green-context 50/50 split), `--arm` the reference cost-model allocate(), `--engine
+hybrid-2048` the same engine's chunked-prefill comparator.
 
 A "step" is one decode iteration of the engine (one CUDA-graph replay over
 the current batch; prefill chunks run concurrently on the other partition).
@@ -18,7 +22,7 @@ the trace so the batch is in steady state), then exactly K timed steps between
 CUDA events on the decode stream. value = output tokens delivered in those K
 steps / their device time (whole-job tokens/s; N ranks -> sum of tokens / max
 window time). The SLO check (pooled p99 ITL <= 50 ms over the run) decides
-whether the point is SLO-constrained. Inputs are larger than L2 (KV cache and
+whether the point is SLO-constrained (--slo-ms). Inputs are larger than L2 (KV cache and
 weights, ~30 GB per step), so no extra flush is needed.
 
 N > 1 (torchrun): one independent replica per GPU ("replicas only"; the path
@@ -43,6 +47,8 @@ sys.path.insert(0, ROOT)
 
 SLO_ITL_US = 50_000
 PROMPT, OUTPUT = 1024, 256
+# measured ARM tables (python -m paper_2601_11822_b200.profiler), per model, at its benchmark mix
+DEFAULT_PROFILES = {"llama3.1-8b": "llama3.1-8b_ctx1152_chunk1023.json", "qwen2.5-14b": "qwen2.5-14b_ctx8256.json"}
 
 
 def _peaks() -> dict:
@@ -178,11 +184,12 @@ def main():
     ap.add_argument("--steps", type=int, default=600)
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    # 40 QPS saturates cfg 2 on one B200 (prefill-bound); with p99 ITL still far under the SLO,
-    # the saturated delivered rate is the SLO-constrained maximum of the QPS sweep.
-    ap.add_argument("--qps", type=float, default=40.0)
+    # 56 QPS (14.3k output tok/s offered) saturates the RAPID engine on one B200 with p99 ITL
+    # under the SLO: the saturated delivered rate is the SLO-constrained maximum of the sweep.
+    ap.add_argument("--qps", type=float, default=56.0)
     ap.add_argument("--duration", type=float, default=None)
-    ap.add_argument("--decode-sms", type=int, default=72)
+    ap.add_argument("--decode-sms", type=int, default=None,
+                    help="cfg 2: static split with this many decode SMs (72 = the green-context 50/50)")
     ap.add_argument("--model", default="llama3.1-8b")
     ap.add_argument("--prompt", type=int, default=PROMPT, help="mean prompt tokens (cfg 5: 8192)")
     ap.add_argument("--output", type=int, default=OUTPUT, help="mean output tokens (cfg 5: 128)")
@@ -190,17 +197,29 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--engine", default="rapid", help="rapid | hybrid-<chunk> (same-engine chunked-prefill comparator)")
     ap.add_argument("--slo-ms", type=float, default=SLO_ITL_US / 1e3, help="p99 ITL SLO (default 50 ms)")
-    ap.add_argument("--arm-profile", default=None,
-                    help="measured B200 ARM tables (profiler.py JSON); implies --arm with arm.MeasuredArm")
-    ap.add_argument("--arm-policy", default="balanced", choices=["balanced", "slo-min", "adaptive"])
+    ap.add_argument("--arm-profile", default="auto",
+                    help="measured B200 ARM tables (profiler.py JSON; 'auto' = the committed profile of --model "
+                         "under profiles/arm/)")
+    ap.add_argument("--arm-policy", default="adaptive", choices=["balanced", "slo-min", "adaptive"])
     ap.add_argument("--arm", action="store_true",
-                    help="cfg 3: adaptive ARM (allocate() per launch) instead of the cfg-2 static split")
+                    help="the reference allocate() on the cost model instead of the measured ARM")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     PROMPT, OUTPUT = args.prompt, args.output
     SLO_ITL_US = int(args.slo_ms * 1e3)
+    # default (cfg 3): RAPID with the measured adaptive ARM; --decode-sms N: cfg-2 static split;
+    # --arm: the reference cost-model allocate()
+    if args.decode_sms is not None or args.arm or args.engine != "rapid":
+        args.arm_profile = None
+    elif args.arm_profile == "auto":
+        args.arm_profile = os.path.join(ROOT, "profiles", "arm", DEFAULT_PROFILES.get(args.model, ""))
+        if not os.path.isfile(args.arm_profile):
+            args.arm_profile = None
+            args.arm = True
     if args.arm_profile:
         args.arm = True
+    if args.decode_sms is None:
+        args.decode_sms = 72
 
     rank, world, local = dist_setup()
     if args.impl == "reference":
@@ -332,11 +351,21 @@ def main():
     value = tokens / (ms / 1e3) if complete else 0.0
     e2e_value = tokens / host_s if complete else 0.0
 
-    # live roofline probe of the dominant decode kernel (decode attention)
+    # live roofline probe of the dominant decode kernel (decode attention) at the window's mean
+    # batch and context: on the static decode partition (cfg 2) or, under the ARM, on all SMs
+    # (the kernel against the device peak) plus the ARM's most frequent decode partition
     part = ex._partitions[pkey]
     mB = int(round(statistics.mean(win["Bs"]))) if win["Bs"] else 64
     mctx = int(round(statistics.mean(win["ctxs"]))) if win["ctxs"] else PROMPT + OUTPUT // 2
     probe = time_decode_attention(ex.runner, part.ds, mB, mctx, part.d_sms)
+    part_probe = None
+    if args.arm and getattr(engine, "decision_log", None) and not hybrid:
+        used = collections.Counter(round(d.cu_fraction_decode * total) for ph, d in engine.decision_log
+                                   if ph == "decode" and d.mode.value == "partition")
+        if used:
+            pp = ex._partition(used.most_common(1)[0][0])
+            part_probe = time_decode_attention(ex.runner, pp.ds, mB, mctx, pp.d_sms)
+            part_probe["sms"] = pp.d_sms
     hbm = peaks["hbm_gbs"]
     # DRAM traffic of the dominant kernel from the committed ncu --set full capture, per launch:
     # measured bytes / algorithmic bytes at the capture shape, times this probe's algorithmic bytes
@@ -420,7 +449,11 @@ def main():
                      "traffic_src": "profiles/ncu_traffic.json (dram read+write / algorithmic bytes of one "
                                     "ncu --set full launch, scaled to this probe)",
                      "per_launch": f"B={probe['B']} ctx={probe['ctx']}: {probe['bytes']} B (K+V bf16, 1 layer) "
-                                   f"in {probe['ms'] * 1e3:.1f} us on the {d_sms}-SM decode partition",
+                                   f"in {probe['ms'] * 1e3:.1f} us on {part.d_sms} SMs",
+                     "on_arm_partition": (None if part_probe is None else
+                                          {"sms": part_probe["sms"], "achieved": part_probe["gbs"],
+                                           "frac": part_probe["gbs"] / hbm,
+                                           "us": round(part_probe["ms"] * 1e3, 1)}),
                      "peak_src": peaks["_src"]},
         "gpu_launches": launches,
         "clocks": win.get("clocks", {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}),
