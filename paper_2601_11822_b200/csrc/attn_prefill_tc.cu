@@ -16,9 +16,11 @@
 //             O_j = P_j V_j   (M=128, N=128, K=64;  B = V MN-major)  -> TMEM O[j%2]
 //           S_{j+1} is issued before O_j so QK^T overlaps the softmax.
 //   w2..w5  softmax (thread = query row = TMEM lane): S row -> mask, running
-//           max/sum (exp2) -> P row (bf16) into smem in the UMMA K-major
-//           layout -> after O_j lands, o = o*alpha + O_j in registers.
-// Output row = o / l, written straight from registers (256 B per row).
+//           max/sum (exp2) -> P row (bf16) into smem in the UMMA K-major layout.
+// O accumulates in TMEM across all key tiles (PV_j with accumulate). The softmax
+// keeps a stale row max and rescales the TMEM O row (ld, scale, st) only when the
+// max grows by more than kRescaleLog2 (P <= 2^8 otherwise): no per-tile O fold.
+// Output row = O / l, read from TMEM once at the end (256 B per row).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
@@ -39,8 +41,9 @@ constexpr int kKVHalf = kBN * 128;         // 8 KB: 64 keys x 64 dims
 constexpr int kKVStage = 4 * kKVHalf;      // K lo, K hi, V lo, V hi = 32 KB
 constexpr int kPBytes = kBMq * kBN * 2;    // 16 KB
 constexpr int kThreads = 192;
-constexpr int kTmemCols = 512;             // S[2] x 64 + O[2] x 128 = 384 -> 512
+constexpr int kTmemCols = 256;             // S[2] x 64 + O x 128
 constexpr uint32_t kSCol = 0, kOCol = 128;
+constexpr float kRescaleLog2 = 8.0f;       // rescale O only when the row max grows by > 2^8
 }  // namespace fa
 
 // K-major SW128 descriptor with explicit SBO (atoms of 8 rows x 128 B)
@@ -73,6 +76,12 @@ __device__ __forceinline__ void tma_load_3d(void* dst_smem, const void* tmap, ui
       : "memory");
 }
 
+__device__ __forceinline__ float ex2_approx(float x) {  // MUFU.EX2; ex2(-inf) = +0
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ void tmem_ld_x32(uint32_t taddr, float (&v)[32]) {
   uint32_t r[32];
   tmem_ld_32x32b_x32(taddr, r);
@@ -102,8 +111,7 @@ __global__ void __launch_bounds__(fa::kThreads, 1)
   uint64_t* p_full = s_free + 2;
   uint64_t* p_free = p_full + 2;
   uint64_t* o_full = p_free + 2;
-  uint64_t* o_free = o_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 4);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -128,7 +136,6 @@ __global__ void __launch_bounds__(fa::kThreads, 1)
       mbar_init(&p_full[b], 4);
       mbar_init(&p_free[b], 1);
       mbar_init(&o_full[b], 1);
-      mbar_init(&o_free[b], 4);
     }
     fence_barrier_init();
   }
@@ -197,8 +204,7 @@ __global__ void __launch_bounds__(fa::kThreads, 1)
         const int st = j % kStages;
         const int b = j & 1;
         const uint32_t ph2 = (uint32_t)((j >> 1) & 1);
-        mbar_wait(&p_full[b], ph2);
-        mbar_wait(&o_free[b], ph2 ^ 1);
+        mbar_wait(&p_full[b], ph2);  // also orders any O rescale the softmax warps did
         tc_fence_after();
         const uint32_t pa = smem_u32(sP + (size_t)b * kPBytes);
         const uint32_t vb = smem_u32(sKV + (size_t)st * kKVStage + 2 * kKVHalf);
@@ -206,7 +212,7 @@ __global__ void __launch_bounds__(fa::kThreads, 1)
         for (int kk = 0; kk < kBN / 16; ++kk) {
           const uint64_t ad = sdesc_kmajor(pa + kk * 32);
           const uint64_t bd = sdesc_mnmajor(vb + kk * 2048, kKVHalf);
-          umma_bf16(tmem + kOCol + (uint32_t)b * kD, ad, bd, idesc_o, kk > 0 ? 1u : 0u);
+          umma_bf16(tmem + kOCol, ad, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
         }
         umma_commit(&o_full[b]);
         umma_commit(&p_free[b]);
@@ -219,27 +225,8 @@ __global__ void __launch_bounds__(fa::kThreads, 1)
     const int row = qd * 32 + lane;
     const int qpos = start + q0 + row;
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
-    float o[kD];
-#pragma unroll
-    for (int i = 0; i < kD; ++i) o[i] = 0.f;
-    float m = -FLT_MAX, l = 0.f;
-    float alpha_prev = 1.f;
-    // o <- o * alpha_jj + O_jj, where alpha_jj rescales o (relative to m_{jj-1}) to m_jj
-    auto fold_o = [&](int jj, float a) {
-      const int bb = jj & 1;
-      mbar_wait(&o_full[bb], (uint32_t)((jj >> 1) & 1));
-      tc_fence_after();
-#pragma unroll
-      for (int cc = 0; cc < kD / 32; ++cc) {
-        float t[32];
-        tmem_ld_x32(tmem + lane_off + kOCol + (uint32_t)bb * kD + cc * 32, t);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) o[cc * 32 + i] = o[cc * 32 + i] * a + t[i];
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&o_free[bb]);
-    };
+    const uint32_t o_taddr = tmem + lane_off + kOCol;
+    float m = -INFINITY, l = 0.f;  // m: the (stale) max P is taken against
     for (int j = 0; j < n_tiles; ++j) {
       const int b = j & 1;
       const uint32_t ph2 = (uint32_t)((j >> 1) & 1);
@@ -247,38 +234,78 @@ __global__ void __launch_bounds__(fa::kThreads, 1)
       tc_fence_after();
       float s[kBN];
       {
-        float t0[32], t1[32];
-        tmem_ld_x32(tmem + lane_off + kSCol + (uint32_t)b * kBN, t0);
-        tmem_ld_x32(tmem + lane_off + kSCol + (uint32_t)b * kBN + 32, t1);
+        uint32_t t0[32], t1[32];
+        tmem_ld_32x32b_x32(tmem + lane_off + kSCol + (uint32_t)b * kBN, t0);
+        tmem_ld_32x32b_x32(tmem + lane_off + kSCol + (uint32_t)b * kBN + 32, t1);
+        tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          s[i] = t0[i];
-          s[32 + i] = t1[i];
+          s[i] = __uint_as_float(t0[i]);
+          s[32 + i] = __uint_as_float(t1[i]);
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_free[b]);
       const int kbase = j * kBN;
-      float mx = -FLT_MAX;
+      // masked scores are -inf (exp2 -> 0 with no select); tile 0 always holds key 0 <= qpos,
+      // so the max is finite from the first tile on. Only tiles crossing this row's diagonal
+      // or the chunk end need the per-key mask.
+      float mx = -INFINITY;
+      if (kbase + kBN - 1 <= qpos && kbase + kBN <= kv_end) {
 #pragma unroll
-      for (int i = 0; i < kBN; ++i) {
-        const int kp = kbase + i;
-        const float v = (kp > qpos || kp >= kv_end) ? -FLT_MAX : s[i] * scale_log2;
-        s[i] = v;
-        mx = fmaxf(mx, v);
+        for (int i = 0; i < kBN; ++i) {
+          s[i] *= scale_log2;
+          mx = fmaxf(mx, s[i]);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < kBN; ++i) {
+          const int kp = kbase + i;
+          const float v = (kp > qpos || kp >= kv_end) ? -INFINITY : s[i] * scale_log2;
+          s[i] = v;
+          mx = fmaxf(mx, v);
+        }
       }
-      const float mn = fmaxf(m, mx);
-      const float alpha = (mn == -FLT_MAX) ? 1.f : exp2f(m - mn);
-      m = mn;
+      // warp-uniform decision (tcgen05.ld/st below are warp-collective): when any row's stale
+      // max is too far behind, every row of the warp moves its max up and rescales l and O
+      if (__any_sync(0xffffffffu, mx > m + kRescaleLog2)) {
+        const float mn = fmaxf(m, mx);
+        const float alpha = ex2_approx(m - mn);  // tile 0: m = -inf -> 0 (l and O still empty)
+        l *= alpha;
+        if (j > 0) {
+          // O holds PV_0..PV_{j-1}: wait for the last of them, then O_row *= alpha in TMEM.
+          // (PV_{j+1} cannot run before this warp's p_full(j+1), so the barrier is at most one
+          // phase past the one waited for.)
+          mbar_wait(&o_full[(j - 1) & 1], (uint32_t)(((j - 1) >> 1) & 1));
+          tc_fence_after();
+#pragma unroll
+          for (int cc = 0; cc < kD / 32; cc += 2) {
+            uint32_t t0[32], t1[32];
+            tmem_ld_32x32b_x32(o_taddr + cc * 32, t0);
+            tmem_ld_32x32b_x32(o_taddr + (cc + 1) * 32, t1);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              t0[i] = __float_as_uint(__uint_as_float(t0[i]) * alpha);
+              t1[i] = __float_as_uint(__uint_as_float(t1[i]) * alpha);
+            }
+            tmem_st_32x32b_x32(o_taddr + cc * 32, t0);
+            tmem_st_32x32b_x32(o_taddr + (cc + 1) * 32, t1);
+          }
+          tmem_st_wait();
+          tc_fence_before();
+        }
+        m = mn;
+      }
       float ps = 0.f;
 #pragma unroll
       for (int i = 0; i < kBN; ++i) {
-        const float p = (s[i] == -FLT_MAX) ? 0.f : exp2f(s[i] - mn);
+        const float p = ex2_approx(s[i] - m);
         s[i] = p;
         ps += p;
       }
-      l = l * alpha + ps;
+      l += ps;
       // P row -> smem (K-major SW128: row r at (r/8)*1024 + (r%8)*128, 16-B chunk c at c ^ (r%8))
       mbar_wait(&p_free[b], ph2 ^ 1);
       uint8_t* prow = sP + (size_t)b * kPBytes + (row >> 3) * 1024 + (row & 7) * 128;
@@ -304,20 +331,27 @@ __global__ void __launch_bounds__(fa::kThreads, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[b]);
-      // fold O_{j-1} (computed by the tensor cores while this tile's softmax ran)
-      if (j > 0) fold_o(j - 1, alpha_prev);
-      alpha_prev = alpha;
     }
-    if (n_tiles > 0) fold_o(n_tiles - 1, alpha_prev);
+    if (n_tiles > 0) {
+      mbar_wait(&o_full[(n_tiles - 1) & 1], (uint32_t)(((n_tiles - 1) >> 1) & 1));
+      tc_fence_after();
+    }
     const int trow = q0 + row;
-    if (trow < T) {
-      const float inv = l > 0.f ? 1.f / l : 0.f;
-      __nv_bfloat16* dst = out + (size_t)trow * out_tok_stride + (size_t)hq * kD;
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat16* dst = out + (size_t)trow * out_tok_stride + (size_t)hq * kD;
 #pragma unroll
-      for (int c = 0; c < kD / 8; ++c) {
-        reinterpret_cast<uint4*>(dst)[c] =
-            make_uint4(pack_bf16x2(o[8 * c] * inv, o[8 * c + 1] * inv), pack_bf16x2(o[8 * c + 2] * inv, o[8 * c + 3] * inv),
-                       pack_bf16x2(o[8 * c + 4] * inv, o[8 * c + 5] * inv), pack_bf16x2(o[8 * c + 6] * inv, o[8 * c + 7] * inv));
+    for (int cc = 0; cc < kD / 32; ++cc) {
+      uint32_t t[32];
+      tmem_ld_32x32b_x32(o_taddr + cc * 32, t);  // warp-collective: every lane loads, valid rows store
+      tmem_ld_wait();
+      if (trow < T) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          reinterpret_cast<uint4*>(dst + cc * 32)[c] = make_uint4(
+              pack_bf16x2(__uint_as_float(t[8 * c]) * inv, __uint_as_float(t[8 * c + 1]) * inv),
+              pack_bf16x2(__uint_as_float(t[8 * c + 2]) * inv, __uint_as_float(t[8 * c + 3]) * inv),
+              pack_bf16x2(__uint_as_float(t[8 * c + 4]) * inv, __uint_as_float(t[8 * c + 5]) * inv),
+              pack_bf16x2(__uint_as_float(t[8 * c + 6]) * inv, __uint_as_float(t[8 * c + 7]) * inv));
       }
     }
   }

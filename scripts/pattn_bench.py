@@ -1,20 +1,31 @@
-"""Prefill attention timing (graph-timed) at cfg shapes."""
-import json, os, sys
+"""Prefill attention (K2 tcgen05) time for one chunk: T tokens after a prefix, Llama-8B heads."""
+import json
+import os
+import sys
+
 import torch
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2601_11822_b200 import ops  # noqa
-from scripts.kbench import timeit  # noqa
-dev = "cuda"
-for (T, start, Hq, Hkv) in [(1023, 0, 32, 8), (2048, 0, 32, 8), (2048, 6144, 40, 8), (2048, 0, 40, 8)]:
-    nb = (start + T + 15) // 16 + 4
-    cache = torch.randn(nb, 2, Hkv, 16, 128, device=dev).bfloat16()
-    bt = torch.arange(nb, dtype=torch.int32, device=dev)
-    q = torch.randn(T, Hq, 128, device=dev).bfloat16()
+from paper_2601_11822_b200 import ops  # noqa: E402
+
+ops.load()
+Hq, Hkv, D = 32, 8, 128
+for T, start in [(1023, 0), (2048, 0), (2048, 6144)]:
+    n = start + T
+    npg = (n + 15) // 16
+    cache = torch.randn(npg + 8, 2, Hkv, 16, D, device="cuda").bfloat16()
+    bt = torch.arange(npg, dtype=torch.int32, device="cuda")
+    q = torch.randn(T, Hq, D, device="cuda").bfloat16()
     out = torch.empty_like(q)
-    flops = 4 * Hq * 128 * (T * T / 2 + T * start)
-    row = dict(T=T, start=start, Hq=Hq, Hkv=Hkv)
-    for impl in ("mma", "tc"):
-        ms = timeit(lambda: ops.prefill_attention(q, cache, bt, start, out, num_kv_heads=Hkv, impl=impl))
-        row[impl + "_us"] = round(ms * 1e3, 1)
-        row[impl + "_tflops"] = round(flops / ms / 1e9, 1)
-    print(json.dumps(row))
+    for _ in range(2):
+        ops.prefill_attention(q, cache, bt, start, out, num_kv_heads=Hkv)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(10):
+        ops.prefill_attention(q, cache, bt, start, out, num_kv_heads=Hkv)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / 10
+    fl = 4 * Hq * D * (T * T / 2 + T * start)
+    print(json.dumps({"T": T, "start": start, "us": round(ms * 1e3, 1), "tflops": round(fl / ms / 1e9, 1)}))

@@ -198,6 +198,30 @@ def test_prefill_attention(T, start, Hq, Hkv, impl):
     assert rel_l2(out, ref) < 1e-2
 
 
+@pytest.mark.parametrize("T,start", [(300, 0), (200, 333)])
+def test_prefill_attention_growing_max(T, start):
+    """Scores that grow along the keys force the tcgen05 kernel's lazy O rescale (row max
+    rising by more than 2^8 after the first tile, in some rows of a warp but not others)."""
+    gen = torch.Generator(device=DEV).manual_seed(T + 7 * start)
+    D, nb, Hq, Hkv = 128, 128, 8, 2
+    cache = _make_cache(nb, Hkv, D, gen)
+    bt_row = torch.randperm(nb, device=DEV, generator=gen).int()[:48].contiguous()
+    n = start + T
+    q = torch.randn(T, Hq, D, device=DEV, generator=gen)
+    q[::3] *= 0.05  # some rows barely move their max: a warp's rows disagree on rescaling
+    q = q.bfloat16()
+    pages = bt_row[: (n + 15) // 16].long()
+    ramp = torch.linspace(0.2, 6.0, (n + 15) // 16 * 16, device=DEV).view(-1, 1, 16, 1)
+    k = cache[pages, 0].float() * ramp  # [pages, Hkv, 16, D]: later keys score much higher
+    cache[pages, 0] = k.bfloat16()
+    out = torch.empty(T, Hq, D, device=DEV, dtype=torch.bfloat16)
+    ops.prefill_attention(q, cache, bt_row, start, out, num_kv_heads=Hkv, impl="tc")
+    torch.cuda.synchronize()
+    kk, vv = _gather_kv(cache, bt_row, n)
+    assert torch.isfinite(out).all()
+    assert rel_l2(out, _ref_attn(q, kk, vv, causal_offset=start)) < 1e-2
+
+
 @pytest.mark.parametrize("impl", ["tc", "mma"])
 def test_prefill_attention_stale_nan_tail(impl):
     """Slots after the chunk end in its last page may never have been written."""
