@@ -182,13 +182,15 @@ def test_decode_attention_padded_rows():
 
 @pytest.mark.parametrize("impl", ["tc", "mma"])
 @pytest.mark.parametrize("T,start,Hq,Hkv", [(100, 0, 8, 2), (64, 37, 8, 2), (200, 130, 32, 8), (1, 50, 40, 8),
-                                            (257, 0, 8, 1), (300, 500, 32, 8)])
+                                            (257, 0, 8, 1), (300, 500, 32, 8), (1100, 0, 8, 2), (1300, 700, 8, 2)])
 def test_prefill_attention(T, start, Hq, Hkv, impl):
+    # (1100, 0): 9 query tiles from position 0 -> one tile per CTA in the tcgen05 kernel; the
+    # others run two tiles per CTA (paired warpgroups sharing K/V)
     gen = torch.Generator(device=DEV).manual_seed(T + start)
     D, nb = 128, 256
     cache = _make_cache(nb, Hkv, D, gen)
-    bt_row = torch.randperm(nb, device=DEV, generator=gen).int()[:64].contiguous()
-    assert (start + T + 15) // 16 <= 64
+    bt_row = torch.randperm(nb, device=DEV, generator=gen).int()[:160].contiguous()
+    assert (start + T + 15) // 16 <= 160
     q = torch.randn(T, Hq, D, device=DEV, generator=gen).bfloat16()
     out = torch.empty(T, Hq, D, device=DEV, dtype=torch.bfloat16)
     ops.prefill_attention(q, cache, bt_row, start, out, num_kv_heads=Hkv, impl=impl)
