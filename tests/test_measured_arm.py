@@ -108,3 +108,26 @@ def test_adaptive_policy_walks_with_queue_feedback():
     assert set(mp.ladder[max(0, i - arm.SPAN):i + arm.SPAN + 1]) <= arm.splits_used()
     # idle phases still overallocate
     assert arm.decide(0, 100, 0.25).mode is AllocationMode.OVERALLOCATE
+
+
+@pytest.mark.parametrize("name", ["llama3.1-8b_ctx1152_chunk1023.json", "qwen2.5-14b_ctx8256.json"])
+def test_committed_b200_profiles(name):
+    """The measured tables bench.py serves with by default: well-formed, monotone in the
+    ways the policy relies on, and every decision they drive fits the SLO target."""
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.dirname(__file__)), "profiles", "arm", name)
+    mp = MeasuredProfile.load(path)
+    assert mp.total == 148 and len(mp.ladder) >= 8
+    # more decode SMs never make the (measured) step much slower
+    for b in mp.batches:
+        steps = [mp.decode_us(d, b) for d in mp.ladder]
+        assert all(steps[i + 1] <= steps[i] * 1.15 for i in range(len(steps) - 1)), (b, steps)
+    for policy in ("balanced", "adaptive", "slo-min"):
+        arm = MeasuredArm(mp, 50_000, max_batch=256, policy=policy)
+        for b in mp.batches:
+            d = decode_sms_of(arm.decide(b, 2048, 0.25), 148)
+            if policy != "slo-min" and d is not None and arm.candidates(b):
+                assert mp.decode_us(d, b) <= arm.target
+    lines = profile_lines(mp.to_profile(50_000))
+    assert len(lines) == len(mp.batches)
