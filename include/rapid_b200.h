@@ -69,7 +69,9 @@ int rb_gemm_bf16(const void* X, const void* W, void* Y, const void* bias, const 
  * ceil(seq_lens[b]/16) over the launch (sequences are cut into 16-page work
  * items, whole sequences when B*Hkv fills the partition); when sequences are
  * split the workspace must hold B*Hq*splits*(head_dim+2)*4 bytes of partials
- * (splits <= ceil(max_pages/8)). num_blocks = pages in the
+ * (splits <= ceil(max_pages/8)). The last 64 bytes of a non-NULL workspace hold
+ * self-resetting work counters (items are handed to warps dynamically) and must be
+ * zero before the first call. num_blocks = pages in the
  * cache layer (TMA extent); num_sms = SMs of the launching partition. */
 int rb_decode_attention(const void* q, long long q_tok_stride, const void* cache_layer, const int* block_table,
                         int bt_stride, const int* row_slot, const int* seq_lens, void* out,

@@ -33,8 +33,8 @@ namespace rb {
 
 constexpr int kD = 128;
 constexpr int kPage = 16;
-constexpr int kWarps = 8;
-constexpr int kStages = 3;
+// (warps per CTA, smem stages per warp): 8 x 3 on large partitions; 12 x 2 on <= 64-SM
+// partitions, where more warps in flight per SM measured up to +35% (56 SMs, B=226)
 constexpr int kStageBytes = 4 * 2048;     // K lo/hi + V lo/hi, 16 rows x 128 B each
 constexpr int kPStageBytes = 256;         // P^T staging per warp
 
@@ -76,7 +76,10 @@ struct DecArgs {
   float* part_ml;  // [items][G][2]
   int B, Hkv, G, splits, chunk_pages;
   float scale_log2;
+  int* work;  // [2] self-resetting (next item, finished warps): dynamic item assignment; null = static
 };
+
+constexpr int kQueue = 8;  // per-warp ring of acquired item ids (producer lane 0 -> all lanes)
 
 // decode an item index -> (b, h, chunk); returns pages [p0, p1) (empty if past the sequence)
 __device__ __forceinline__ void item_pages(const DecArgs& a, int item, int& b, int& h, int& c, int& p0, int& p1,
@@ -91,6 +94,7 @@ __device__ __forceinline__ void item_pages(const DecArgs& a, int item, int& b, i
   p1 = min(nb, p0 + a.chunk_pages);
 }
 
+template <int kWarps, int kStages>
 __global__ void __launch_bounds__(kWarps * 32, 1)
     decode_attn_tc_kernel(const __grid_constant__ CUtensorMap kv_map, const DecArgs a) {
   pdl_trigger();
@@ -103,6 +107,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   uint8_t* pst = smem + (size_t)kWarps * kStages * kStageBytes + warp * kPStageBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kWarps * kStages * kStageBytes +
                                                kWarps * kPStageBytes) + warp * kStages;
+  int* queue = reinterpret_cast<int*>(reinterpret_cast<uint64_t*>(smem + (size_t)kWarps * kStages * kStageBytes +
+                                                                  kWarps * kPStageBytes) + kWarps * kStages) +
+               warp * kQueue;
   if (lane == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
     fence_barrier_init();
@@ -116,14 +123,24 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   const int g = lane >> 2;  // group id (row of the fragment)
   const int t = lane & 3;
 
-  // ---------------- producer cursor (lane 0): next page to fetch
-  int pi = gw, pp = 0, pp1 = 0, pb = 0, ph = 0, pc = 0, pn = 0;
-  auto p_seek = [&]() {  // advance pi to an item with pages; sets pp..pp1
+  // ---------------- producer cursor (lane 0): next page to fetch. Items come from a global
+  // atomic counter when a.work is set (warps that finish early take more: no tail from the
+  // items-per-warp quantization), else statically gw, gw + nw, ... The producer runs ahead of
+  // the consumer across item boundaries, so each acquired item id (and a final -1) goes
+  // through a per-warp smem ring in acquisition order.
+  int qtail = 0;
+  auto next_item = [&](int cur) { return a.work ? atomicAdd(&a.work[0], 1) : cur + nw; };
+  int pi = a.work ? -1 : gw, pp = 0, pp1 = 0, pb = 0, ph = 0, pc = 0, pn = 0;
+  auto p_seek = [&]() {  // advance pi to an item with pages; sets pp..pp1 and enqueues it
     while (pi < total_items) {
       item_pages(a, pi, pb, ph, pc, pp, pp1, pn);
-      if (pp < pp1) return;
-      pi += nw;
+      if (pp < pp1) {
+        queue[qtail++ & (kQueue - 1)] = pi;
+        return;
+      }
+      pi = next_item(pi);
     }
+    queue[qtail++ & (kQueue - 1)] = -1;
   };
   int issued = 0;
   auto p_issue = [&](int stage) {
@@ -138,11 +155,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     tma_load_2d(dst + 4096, &kv_map, &bars[stage], 0, rowV, kEvictFirst);
     tma_load_2d(dst + 6144, &kv_map, &bars[stage], 64, rowV, kEvictFirst);
     if (++pp == pp1) {
-      pi += nw;
+      pi = next_item(pi);
       p_seek();
     }
   };
   if (lane == 0) {
+    if (a.work) pi = atomicAdd(&a.work[0], 1);
     p_seek();
     for (int s = 0; s < kStages && pi < total_items; ++s) {
       p_issue(s);
@@ -152,10 +170,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 
   int stage = 0;
   uint32_t phase = 0;
-  for (int item = gw; item < total_items; item += nw) {
+  for (int qhead = 0;; ++qhead) {
+    __syncwarp();  // lane 0's queue writes are visible to the warp
+    const int item = queue[qhead & (kQueue - 1)];
+    if (item < 0) break;
     int b, h, c, p0, p1, n;
     item_pages(a, item, b, h, c, p0, p1, n);
-    if (p0 >= p1) continue;
     // Q^T fragments (B operand): b0 = (dims 16kk+2t.., head g), b1 = (dims 16kk+8+2t.., head g)
     uint32_t qb[8][2];
     {
@@ -297,6 +317,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       }
     }
   }
+  // re-arm the work counter for the next launch / graph replay: the last warp to finish resets it
+  // (every warp has drawn its final, out-of-range ticket before it counts itself done)
+  if (a.work && lane == 0) {
+    if (atomicAdd(&a.work[1], 1) == nw - 1) {
+      a.work[0] = 0;
+      a.work[1] = 0;
+      __threadfence();
+    }
+  }
 }
 
 // merges the chunk partials of multi-chunk sequences; grid (B, Hq), 128 threads
@@ -344,13 +373,25 @@ int decode_attention_launch(const void* q, long long q_tok_stride, const void* c
   // Work-item size: whole sequences when (B x Hkv) already gives every warp of the
   // partition at least one item (no partials, no combine pass); otherwise cut sequences into
   // chunks so there are ~4 items per warp (load balance for long contexts / small B).
+  const bool small = num_sms <= 100;
+  const int kWarps = small ? 12 : 8;
+  const int kStages = small ? 2 : 3;
   const long long warps = (long long)num_sms * kWarps;
   const long long seqs = (long long)B * Hkv;
   int chunk_pages = max_pages;
-  if (seqs < warps) {
+  // small partitions are bound per SM: fewer than ~1.5 whole sequences per warp leaves a
+  // ragged last round even with dynamic assignment, so cut sequences there too
+  if (seqs < warps || (small && 2 * seqs < 3 * warps)) {
     chunk_pages = (int)((max_pages * seqs + 4 * warps - 1) / (4 * warps));
     if (chunk_pages < 8) chunk_pages = 8;
     if (chunk_pages > max_pages) chunk_pages = max_pages;
+  }
+  // the last 64 bytes of the workspace hold the self-resetting work counters (zero before the
+  // first call); the partials use the rest
+  int* work = nullptr;
+  if (workspace != nullptr && ws_bytes >= 64) {
+    work = reinterpret_cast<int*>(static_cast<char*>(workspace) + ((ws_bytes - 64) & ~size_t(63)));
+    ws_bytes = (ws_bytes - 64) & ~size_t(63);
   }
   // splitting is an optimisation: without room for the partials, keep whole sequences
   if ((size_t)B * Hq * ((max_pages + chunk_pages - 1) / chunk_pages) * (kD + 2) * sizeof(float) > ws_bytes ||
@@ -372,6 +413,7 @@ int decode_attention_launch(const void* q, long long q_tok_stride, const void* c
   a.splits = splits;
   a.chunk_pages = chunk_pages;
   a.scale_log2 = scale * 1.4426950408889634f;
+  a.work = work;
   const size_t items = (size_t)B * Hkv * splits;
   if (splits > 1) {
     const size_t need = items * G * (kD + 2) * sizeof(float);
@@ -383,18 +425,21 @@ int decode_attention_launch(const void* q, long long q_tok_stride, const void* c
   const uint64_t rows = (uint64_t)num_blocks * 2 * Hkv * kPage;
   int rc = make_tmap_2d_bf16(&map, cache_layer, kD, rows, kD, 64, kPage);
   if (rc) return rc;
-  const int smem = kWarps * kStages * kStageBytes + kWarps * kPStageBytes + kWarps * kStages * 8 + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(decode_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int smem = kWarps * kStages * kStageBytes + kWarps * kPStageBytes + kWarps * kStages * 8 +
+                   kWarps * kQueue * 4 + 1024;
+  using Fn = void (*)(const CUtensorMap, const DecArgs);
+  const Fn kern = small ? decode_attn_tc_kernel<12, 2> : decode_attn_tc_kernel<8, 3>;
+  static bool attr[2] = {false, false};
+  if (!attr[small]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return set_cuda_error("decode attn smem attr", e);
-    attr = true;
+    attr[small] = true;
   }
   const size_t warps_needed = items;
   int grid = (int)((warps_needed + kWarps - 1) / kWarps);
   if (grid > num_sms) grid = num_sms;
   if (grid < 1) grid = 1;
-  cudaError_t e = launch_k(decode_attn_tc_kernel, dim3(grid), dim3(kWarps * 32), smem, st, 1, map, a);
+  cudaError_t e = launch_k(kern, dim3(grid), dim3(kWarps * 32), smem, st, 1, map, a);
   if (e != cudaSuccess) return set_cuda_error("decode attn launch", e);
   if (splits > 1) {
     e = launch_k(decode_attn_combine_kernel, dim3(B, Hq), dim3(kD), 0, st, 1, a.part_o, a.part_ml, seq_lens, a.out, out_tok_stride, Hkv, G, splits, chunk_pages);

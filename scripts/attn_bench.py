@@ -30,7 +30,7 @@ nbps = (args.ctx + 15) // 16
 nb = Bmax * nbps * 2 + 8
 cache = torch.randn(nb, 2, args.hkv, 16, D, device="cuda").bfloat16()
 bt = torch.randperm(nb - 8, device="cuda")[: Bmax * nbps].int().view(Bmax, nbps)
-ws = torch.empty(Bmax * args.hq * 64 * (D + 2), dtype=torch.float32, device="cuda")
+ws = torch.zeros(Bmax * args.hq * 64 * (D + 2), dtype=torch.float32, device="cuda")
 for sm in [int(s) for s in args.sms.split(",")]:
     if sm >= 148:
         st, n = torch.cuda.Stream(), 148
