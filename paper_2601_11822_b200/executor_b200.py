@@ -236,28 +236,74 @@ class B200Executor:
         return torch.cat([prompt[lo:P], tail])
 
     # ------------------------------------------------------------------ prefill
+    # Device work of a launch as a plain command (tuple of ints / int lists): the single-GPU
+    # executor runs it directly; under tensor parallelism (tp_engine.py) the leader rank also
+    # broadcasts it and every worker rank runs the same command on its shard.
+    command_sink = None  # callable(cmd) or None
+
+    def _partition_key(self, part: _Partition) -> int | None:
+        return next(k for k, v in self._partitions.items() if v is part)
+
+    def run_command(self, cmd) -> _Partition:
+        """Execute one device command (the same on every TP rank); returns its partition."""
+        kind, key = cmd[0], cmd[1]
+        part = self._partitions[key] if key in self._partitions else self._partition(key)
+        if kind == "prefill":
+            _, _, upd, slot, ids, lo, last = cmd
+            st = part.ps
+            self._upd["prefill"].extend(upd)
+            self._flush_updates("prefill", st)
+            if ids:
+                n = len(ids)
+                self._pre_ids_host[:n].copy_(torch.tensor(ids, dtype=torch.int32))
+                with torch.cuda.stream(st):
+                    self._pre_ids_dev[:n].copy_(self._pre_ids_host[:n], non_blocking=True)
+                    self.runner.prefill(slot, self._pre_ids_dev[:n], lo, num_sms=part.p_sms, stream=st.cuda_stream)
+                self.h2d_bytes += 4 * n
+                self.gpu_launches += self.runner.kernels_per_forward(0, n, False, False, False)
+            if last is not None:
+                ops.set_last_token(self.runner.last_tok, slot, value=last, stream=st.cuda_stream)
+                self.gpu_launches += 1
+        elif kind == "decode":
+            _, _, upd, B, bucket, slots, pos, seq = cmd
+            st = part.ds
+            self._upd["decode"].extend(upd)
+            self._flush_updates("decode", st)
+            self._dec_in_host[:, :bucket].copy_(torch.tensor([slots, pos, seq], dtype=torch.int32))
+            with torch.cuda.stream(st):
+                self._dec_in_dev[:, :bucket].copy_(self._dec_in_host[:, :bucket], non_blocking=True)
+                if self.use_graphs:
+                    self._capture(part, bucket).replay()
+                else:
+                    self.runner.decode_body(bucket, num_sms=part.d_sms, max_pages=(max(seq) + PAGE - 1) // PAGE,
+                                            stream=st.cuda_stream)
+                self._dec_out_host[:B].copy_(self.runner.dec.out_ids[:B], non_blocking=True)
+            self.h2d_bytes += 12 * bucket
+            self.d2h_bytes += 4 * B
+            self.gpu_launches += self.runner.kernels_per_forward(bucket, 0, True, False, True)
+        else:
+            raise ValueError(f"unknown device command {kind!r}")
+        return part
+
+    def _issue(self, cmd) -> _Partition:
+        if self.command_sink is not None:
+            self.command_sink(cmd)
+        return self.run_command(cmd)
+
+    def _take_updates(self, phase: str) -> list:
+        upd = list(self._upd[phase])
+        self._upd[phase].clear()
+        return upd
+
     def launch_prefill(self, req, written: int, chunk: int, target: int, decision, co_decode) -> GpuHandle:
         part = self._pick(decision)
-        st = part.ps
-        sh = st.cuda_stream
-        h = GpuHandle("prefill", st, part.p_sms / self.total_sms)
-        self._flush_updates("prefill", st)
+        h = GpuHandle("prefill", part.ps, part.p_sms / self.total_sms)
         slot = self._slot_of[req.id]
         lo, hi = written, min(written + chunk, target - 1)
-        if hi > lo:
-            ids = self._context_ids(req, lo, hi)
-            n = hi - lo
-            self._pre_ids_host[:n].copy_(ids)
-            with torch.cuda.stream(st):
-                self._pre_ids_dev[:n].copy_(self._pre_ids_host[:n], non_blocking=True)
-                self.runner.prefill(slot, self._pre_ids_dev[:n], lo, num_sms=part.p_sms, stream=sh)
-            self.h2d_bytes += 4 * n
-            self.gpu_launches += self.runner.kernels_per_forward(0, n, False, False, False)
-        if written + chunk == target:
-            nxt = int(self._context_ids(req, target - 1, target)[0])
-            ops.set_last_token(self.runner.last_tok, slot, value=nxt, stream=sh)
-            self.gpu_launches += 1
-        h.finish_record(st)
+        ids = self._context_ids(req, lo, hi).tolist() if hi > lo else []
+        last = int(self._context_ids(req, target - 1, target)[0]) if written + chunk == target else None
+        self._issue(("prefill", self._partition_key(part), self._take_updates("prefill"), slot, ids, lo, last))
+        h.finish_record(part.ps)
         h.req = req
         self.prefill_chunks += 1
         return h
@@ -307,12 +353,9 @@ class B200Executor:
 
     def launch_decode(self, members, decision, co_prefill_chunk) -> GpuHandle:
         part = self._pick(decision)
-        st = part.ds
         B = len(members)
         bucket = self._bucket(B)
-        h = GpuHandle("decode", st, part.d_sms / self.total_sms)
-        self._flush_updates("decode", st)
-        hin = self._dec_in_host
+        h = GpuHandle("decode", part.ds, part.d_sms / self.total_sms)
         slots, pos, seq = [], [], []
         lame = []
         for r in members:
@@ -326,22 +369,11 @@ class B200Executor:
             slots += [self.runner.dummy_slot] * pad
             pos += [-1] * pad
             seq += [0] * pad
-        hin[:, :bucket].copy_(torch.tensor([slots, pos, seq], dtype=torch.int32))
-        with torch.cuda.stream(st):
-            self._dec_in_dev[:, :bucket].copy_(hin[:, :bucket], non_blocking=True)
-            if self.use_graphs:
-                self._capture(part, bucket).replay()
-            else:
-                self.runner.decode_body(bucket, num_sms=part.d_sms, max_pages=(max(seq) + PAGE - 1) // PAGE,
-                                        stream=st.cuda_stream)
-            self._dec_out_host[:B].copy_(self.runner.dec.out_ids[:B], non_blocking=True)
-        h.finish_record(st)
+        self._issue(("decode", self._partition_key(part), self._take_updates("decode"), B, bucket, slots, pos, seq))
+        h.finish_record(part.ds)
         h.members = tuple(members)
         h.lame = lame
-        self.h2d_bytes += 12 * bucket
-        self.d2h_bytes += 4 * B
         self.decode_steps += 1
-        self.gpu_launches += self.runner.kernels_per_forward(bucket, 0, True, False, True)
         return h
 
     def finish_decode(self, handle) -> None:

@@ -1,0 +1,79 @@
+"""TP serving layer (tp_engine.py) over gloo, world 2: every device command the leader's
+executor runs reaches the worker's executor in the same order with the same payload."""
+
+import os
+
+from paper_2601_11822_b200.tp_engine import CommandChannel, attach_leader, serve_worker, stop_workers
+
+
+class _RecordingExecutor:
+    """Stands in for B200Executor: run_command records; _issue mirrors its sink-then-run order."""
+
+    command_sink = None
+
+    def __init__(self):
+        self.ran = []
+
+    def run_command(self, cmd):
+        self.ran.append(cmd)
+
+    def _issue(self, cmd):
+        if self.command_sink is not None:
+            self.command_sink(cmd)
+        return self.run_command(cmd)
+
+
+def _commands():
+    out = []
+    for i in range(25):
+        if i % 5 == 0:
+            out.append(("prefill", 64 if i % 2 else None, [(i, 0, 3 * i), (i, 1, 3 * i + 1)], i, list(range(i, i + 7)),
+                        0, i + 11 if i % 3 == 0 else None))
+        else:
+            B = 1 + i % 7
+            out.append(("decode", 56, [(i, 4, 100 + i)] if i % 4 == 0 else [], B, 8, list(range(8)),
+                        [i] * B + [-1] * (8 - B), [i + 1] * B + [0] * (8 - B)))
+    return out
+
+
+def _rank(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ch = CommandChannel()
+    ex = _RecordingExecutor()
+    if rank == 0:
+        attach_leader(ex, ch)
+        for cmd in _commands():
+            ex._issue(cmd)
+        stop_workers(ch)
+        q.put((rank, ex.ran, ch.sent))
+    else:
+        n = serve_worker(ex, ch)
+        q.put((rank, ex.ran, n))
+    dist.destroy_process_group()
+
+
+def test_leader_commands_replay_on_worker():
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (_, leader_ran, sent), (_, worker_ran, n) = out
+    want = _commands()
+    assert leader_ran == want
+    assert worker_ran == want
+    assert n == len(want) and sent == len(want) + 1  # + STOP
