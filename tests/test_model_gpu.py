@@ -240,3 +240,56 @@ def test_hybrid_realtime_end_to_end_matches_oracle(tiny):
     print(f"hybrid teacher-forced: {exact} exact, {flips} near-tie flips")
     assert flips <= 0.1 * (exact + flips), (exact, flips)
     ex.close()
+
+
+def test_rapid_measured_arm_resplits_keep_oracle_parity(tiny):
+    """RAPID driven by the measured-table ARM (arm.MeasuredArm) on a profile that moves the
+    decode partition with the batch (and OVERALLOCATEs when a phase idles): launches hop
+    between green-context splits mid-request, and every generated token must still pass
+    the oracle check (the shared KV cache and slot state survive the re-splits)."""
+    from paper_2601_11822_b200.arm import DEFAULT_BATCH_GRID, CostParams, MeasuredArm, MeasuredProfile
+    from paper_2601_11822_b200.engines.rapid import RapidEngine
+    from paper_2601_11822_b200.executor_b200 import B200Executor
+    from paper_2601_11822_b200.harness import run_items
+    from paper_2601_11822_b200.slo import SloSpec
+    from paper_2601_11822_b200.specs import b200_spec
+    from paper_2601_11822_b200.traffic import WorkloadSpec, prompt_token_ids, synthesize
+
+    arch, st, orc, w = tiny
+    ladder = (16, 32, 48, 64)
+    # decode step grows with the batch and shrinks with SMs: batch 1 fits the target on 16 SMs,
+    # <= 2 on 32, <= 4 on 48, larger batches need 64
+    dec = {str(d): {str(b): (48_000.0 if b > {16: 1, 32: 2, 48: 4, 64: 256}[d] else 1_000.0)
+                    for b in DEFAULT_BATCH_GRID} for d in ladder}
+    prof = MeasuredProfile({"model": "tiny", "ctx": 128, "chunk": 32, "total_sms": 148, "granularity": 8,
+                            "batches": list(DEFAULT_BATCH_GRID), "decode_us": dec,
+                            "prefill_us_per_token": {str(d): 10.0 + d / 10 for d in ladder},
+                            "overalloc_decode_us": {str(b): 60_000.0 for b in DEFAULT_BATCH_GRID},
+                            "overalloc_prefill_us_per_token": 9.0})
+    slo = SloSpec(itl_slo_us=50_000)
+    policy = MeasuredArm(prof, slo.itl_slo_us, max_batch=32, policy="slo-min")
+    from paper_2601_11822_b200.traffic import WorkloadItem
+
+    # a burst: prefills stay queued while the decode batch grows through the thresholds
+    items = [WorkloadItem(1000 + 700 * i, 40 + (7 * i) % 50, 30 + (5 * i) % 20) for i in range(24)]
+    ex = B200Executor(arch, weights=w, max_batch=32, chunk_tokens=32, num_blocks=800, max_context=1024,
+                      num_slots=64)
+    ex.warmup(sorted(policy.splits_used(), key=lambda d: -1 if d is None else d))
+    model = arch.model_spec()
+    eng = lambda: RapidEngine(model, b200_spec(), CostParams(), slo, chunk_tokens=32, max_batch=32,  # noqa: E731
+                              executor=ex, arm_policy=policy, record_decisions=True)
+    res = run_items("rapid", items, model, b200_spec(), CostParams(), slo, engine_factory=eng)
+    splits = {round(d.cu_fraction_decode * 148) for _, d in res.engine.decision_log
+              if d.mode.value == "partition"}
+    assert len(splits) >= 2, f"the profile should move the decode partition, saw {splits}"
+    done = [r for r in res.engine.requests if r.state.value == "finished"]
+    assert len(done) == len(items)
+    exact = flips = 0
+    for r in done:
+        prompt = prompt_token_ids(r.id, r.prompt_tokens, arch.vocab)
+        assert len(ex.generated[r.id]) == r.output_tokens
+        e, f = teacher_forced_check(orc, prompt, ex.generated[r.id])
+        exact += e
+        flips += f
+    assert flips <= 0.1 * (exact + flips), (exact, flips)
+    ex.close()
