@@ -36,6 +36,7 @@ int embed_launch(const int* ids, const int* slot_of_row, const int* last_tok, co
 int argmax_launch(const void* logits, long long ld, int T, int V, int* out, const int* slot_of_row, int* last_tok,
                   const int* row_valid, cudaStream_t st);
 void* tp_gemm_out(void* tp, void* x, const void** residual);
+bool tp_gemm_push(void* tp, GemmPush* out);
 void tp_begin(void* tp);
 int tp_reduce(void* tp, void* x, long long n, cudaStream_t st);
 int tp_argmax(void* tp, const void* logits, long long ld, int T, int V_local, int offset, int* out,
@@ -111,8 +112,11 @@ extern "C" int rb_decoder_forward(const rb_model_t* m, const rb_workspace_t* w, 
     {  // row-parallel under TP: partial -> all-reduce with the residual add
       const void* res = x;
       void* y = tp_gemm_out(tp, x, &res);
+      GemmPush push{};
+      const bool pushed = tp_gemm_push(tp, &push);  // mode 3: the epilogue stores into every rank
       RB_TRY(gemm_bf16_launch(attn, m->wo[l], y, nullptr, res, T, H, Hq * D, Hq * D, Hq * D, H, 0, sms, w->gemm_ws,
-                              w->gemm_ws_bytes, w->gemm_counters, w->gemm_counters_len, st));
+                              w->gemm_ws_bytes, w->gemm_counters, w->gemm_counters_len, st, nullptr,
+                              pushed ? &push : nullptr));
       RB_TRY(tp_reduce(tp, x, (long long)T * H, st));
     }
     RB_TRY(rmsnorm_launch(x, H, m->ln2[l], h, H, T, H, m->rms_eps, st));
@@ -130,8 +134,10 @@ extern "C" int rb_decoder_forward(const rb_model_t* m, const rb_workspace_t* w, 
     {
       const void* res = x;
       void* y = tp_gemm_out(tp, x, &res);
+      GemmPush push{};
+      const bool pushed = tp_gemm_push(tp, &push);
       RB_TRY(gemm_bf16_launch(act, m->wd[l], y, nullptr, res, T, H, I, I, I, H, 0, sms, w->gemm_ws, w->gemm_ws_bytes,
-                              w->gemm_counters, w->gemm_counters_len, st));
+                              w->gemm_counters, w->gemm_counters_len, st, nullptr, pushed ? &push : nullptr));
       RB_TRY(tp_reduce(tp, x, (long long)T * H, st));
     }
   }

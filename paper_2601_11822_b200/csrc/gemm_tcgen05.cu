@@ -69,6 +69,7 @@ struct GemmArgs {
   float* ws;      // stream-K partials [cluster][rank][mt][BN/32][4 warps][8][32 lanes] float4
   int* counters;  // per (tile, rank), self-resetting
   GemmRope rp;    // rp.q_out != nullptr: fused RoPE + paged K/V write epilogue (QKV projection)
+  GemmPush push;  // push.world > 0: tiles go to every TP rank's receive slot (tp.cu mode 3)
   unsigned long long* trace;  // debug timeline: [cta][8] globaltimer stamps of this launch, or null
 };
 
@@ -311,8 +312,15 @@ __device__ __forceinline__ void epi_block(const GemmArgs& g, __nv_bfloat16* stg,
           x[2 * j + 1] += f.y;
         }
       }
-      *reinterpret_cast<uint4*>(dst) = make_uint4(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3]),
-                                                  pack_bf16x2(x[4], x[5]), pack_bf16x2(x[6], x[7]));
+      const uint4 o4 = make_uint4(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3]), pack_bf16x2(x[4], x[5]),
+                                  pack_bf16x2(x[6], x[7]));
+      if (g.push.world) {  // TP push: this tile into every rank's receive slot (NVLink P2P stores)
+        for (int pj = 0; pj < g.push.world; ++pj)
+          *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(g.push.dst[pj]) + (long long)row * g.ldy + col) =
+              o4;
+      } else {
+        *reinterpret_cast<uint4*>(dst) = o4;
+      }
     } else {
       for (int j = 0; j < 8 && col + j < cols_valid; ++j) {
         float y = x[j];
@@ -726,6 +734,16 @@ __global__ void __launch_bounds__(threads_for(kSets), 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (g.push.world && threadIdx.x == 0) {
+    // every output tile of this CTA is stored (bar.sync above); make them visible system-wide,
+    // and the last CTA of the grid tells every rank this GEMM's slot is complete
+    __threadfence_system();
+    if (atomicAdd(g.push.done_local, 1u) == gridDim.x - 1) {
+      *g.push.done_local = 0u;  // re-arm (next launch is stream-ordered after this one)
+      __threadfence_system();
+      for (int pj = 0; pj < g.push.world; ++pj) atomicAdd_system(g.push.arrive[pj], 1u);
+    }
+  }
   if (kPair == 2) cluster_sync();  // the leader's MMAs into the peer's TMEM are done
   if (threadIdx.x == 0) TRACE(6);
   if (warp == 1) {
@@ -771,7 +789,7 @@ int gemm_set_variant(int v) {
 int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, const void* residual, int T,
                      int O, int K, long long ldx, long long ldw, long long ldy, int mode, int num_sms,
                      void* workspace, size_t ws_bytes, int* counters, int counters_len, cudaStream_t stream,
-                     const GemmRope* rope) {
+                     const GemmRope* rope, const GemmPush* push) {
   if (T <= 0 || O <= 0) return 0;
   if (rope && (rope->q_out == nullptr || rope->hd != 128 || O != (rope->hq + 2 * rope->hkv) * 128 ||
                residual != nullptr || (mode & 4) || rope->ld_q % 8 ||
@@ -877,6 +895,11 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
   g.residual = reinterpret_cast<const __nv_bfloat16*>(residual);
   g.bias = reinterpret_cast<const __nv_bfloat16*>(bias);
   if (rope) g.rp = *rope;
+  if (push) {
+    if (glu || residual != nullptr || rope != nullptr)
+      return set_error("gemm: the TP push epilogue takes a plain output (no SwiGLU / residual / RoPE)");
+    g.push = *push;
+  }
   if (g_trace_host) g.trace = g_trace_host + (size_t)(g_trace_launch++ % 16) * 148 * 16;
   if (swap) {
     g.hint_a = kEvictFirst;  // weights stream once

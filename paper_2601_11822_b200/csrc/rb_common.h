@@ -71,10 +71,20 @@ struct GemmRope {
   int hq, hkv, hd;
 };
 
+// TP push epilogue (tp.cu mode 3): the GEMM writes its output tile straight into every
+// rank's receive slot for this rank (peer memory, tile by tile while the GEMM runs); the last
+// CTA to finish raises one arrival in every rank's counter.
+struct GemmPush {
+  int world;        // 0: off
+  void* dst[8];     // rank j's receive slot for this sender (bf16 [rows][ldy])
+  unsigned* arrive[8];
+  unsigned* done_local;  // this GEMM's CTA completion counter (self-resetting)
+};
+
 int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, const void* residual, int T,
                      int O, int K, long long ldx, long long ldw, long long ldy, int mode, int num_sms,
                      void* workspace, size_t ws_bytes, int* counters, int counters_len, cudaStream_t stream,
-                     const GemmRope* rope = nullptr);
+                     const GemmRope* rope = nullptr, const GemmPush* push = nullptr);
 
 }  // namespace rb
 

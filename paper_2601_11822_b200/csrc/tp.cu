@@ -20,6 +20,12 @@
 //          when several ranks share one device, as in the single-GPU tests). Staging is
 //          double-buffered by call parity, so a rank never overwrites a buffer a peer may
 //          still be reading (two flag rounds separate the reuse).
+//   mode 3 (push, GEMM and collective fused): the row-parallel GEMM's epilogue stores every
+//          output tile straight into each rank's receive slot for this sender (NVLink P2P
+//          stores overlapping the remaining tiles' MMAs) and its last CTA raises one arrival
+//          per rank; the reduce kernel waits for `world` arrivals and sums its own receive
+//          slots + the residual — all reads local. Receive buffers and arrival counters are
+//          double-buffered by call parity; the reducer's last CTA re-arms its counter.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
@@ -149,6 +155,53 @@ __global__ void __launch_bounds__(256) tp_ar_add_kernel(const TpPeers p, __nv_bf
   }
 }
 
+// mode 3: x[i] += sum_j recv[j][i] once all `world` senders have arrived; flags[par] counts
+// arrivals, flags[2 + par] this kernel's finished CTAs (the last re-arms both)
+__global__ void __launch_bounds__(256) tp_push_reduce_kernel(const __nv_bfloat16* __restrict__ recv, long long slot,
+                                                             int world, unsigned* flags, __nv_bfloat16* __restrict__ x,
+                                                             long long n, int par) {
+  pdl_trigger();
+  pdl_wait();
+  if (threadIdx.x == 0)
+    while (ld_acquire_sys(flags + par) < (unsigned)world) {
+    }
+  __syncthreads();
+  const long long per = ((n / 8 + gridDim.x - 1) / gridDim.x) * 8;
+  const long long lo = (long long)blockIdx.x * per;
+  const long long hi = lo + per < n ? lo + per : n;
+  for (long long i = lo + threadIdx.x * 8; i < hi; i += blockDim.x * 8) {
+    float acc[8];
+    {
+      const uint4 u = *reinterpret_cast<const uint4*>(x + i);
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = unpack_bf16x2(w[k]);
+        acc[2 * k] = f.x;
+        acc[2 * k + 1] = f.y;
+      }
+    }
+    for (int j = 0; j < world; ++j) {  // fixed sender order: bit-identical on every rank
+      const uint4 u = __ldcv(reinterpret_cast<const uint4*>(recv + j * slot + i));
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = unpack_bf16x2(w[k]);
+        acc[2 * k] += f.x;
+        acc[2 * k + 1] += f.y;
+      }
+    }
+    *reinterpret_cast<uint4*>(x + i) = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
+                                                  pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(flags + 2 + par, 1u) == gridDim.x - 1) {
+    flags[par] = 0u;
+    flags[2 + par] = 0u;
+    __threadfence_system();
+  }
+}
+
 // ------------------------------------------------------------------ vocab-parallel argmax
 // key = (order-preserving bits of the logit) << 32 | (0xffffffff - global index):
 // max over keys = max logit, lowest index among ties (torch.argmax semantics).
@@ -210,9 +263,26 @@ __global__ void argmax_merge_kernel(const TpPeers p, int use_peers, const unsign
 // ------------------------------------------------------------------ forward hooks
 // Row-parallel GEMM output target: peer mode -> this rank's staging buffer (no
 // residual); NCCL mode -> x itself, residual added on rank 0 only.
+// mode 3: the row-parallel GEMM's push arguments for the current call parity (nullptr otherwise)
+bool tp_gemm_push(void* tp_, GemmPush* out) {
+  TpCtx* tp = static_cast<TpCtx*>(tp_);
+  if (!tp || tp->mode != 3 || tp->world <= 1) return false;
+  out->world = tp->world;
+  for (int j = 0; j < tp->world; ++j) {
+    out->dst[j] = tp->peers.part[tp->parity][j] + (size_t)tp->rank * tp->part_elems;
+    out->arrive[j] = tp->peers.flags[j] + tp->parity;
+  }
+  out->done_local = tp->peers.flags[tp->rank] + 4 + tp->parity;
+  return true;
+}
+
 void* tp_gemm_out(void* tp_, void* x, const void** residual) {
   TpCtx* tp = static_cast<TpCtx*>(tp_);
   if (!tp) return x;
+  if (tp->mode == 3 && tp->world > 1) {
+    *residual = nullptr;  // the reduce kernel adds it
+    return x;             // (unused: the push epilogue writes the receive slots)
+  }
   if (tp->mode == 2 && tp->world > 1) {
     *residual = nullptr;
     return tp->peers.part[tp->parity][tp->rank];
@@ -234,6 +304,16 @@ int tp_reduce(void* tp_, void* x, long long n, cudaStream_t st) {
   }
   if (tp->world <= 1) return 0;
   if ((size_t)n > tp->part_elems || n % 8) return set_error("tp: all-reduce exceeds the staging buffers");
+  if (tp->mode == 3) {
+    int blocks = (int)((n + 256 * 8 * 4 - 1) / (256 * 8 * 4));
+    if (blocks > 120) blocks = 120;
+    if (blocks < 1) blocks = 1;
+    cudaError_t e = launch_k(tp_push_reduce_kernel, dim3(blocks), dim3(256), 0, st, 1,
+                             (const __nv_bfloat16*)tp->peers.part[tp->parity][tp->rank], (long long)tp->part_elems,
+                             tp->world, tp->peers.flags[tp->rank], static_cast<__nv_bfloat16*>(x), n, tp->parity);
+    tp->parity ^= 1;
+    return e == cudaSuccess ? 0 : set_cuda_error("tp push reduce launch", e);
+  }
   int blocks = (int)((n + 256 * 8 * 4 - 1) / (256 * 8 * 4));
   if (blocks > kMaxArBlocks - 1) blocks = kMaxArBlocks - 1;  // the last flag slot belongs to the argmax merge
   if (blocks < 1) blocks = 1;
@@ -299,10 +379,10 @@ int rb_tp_create(int world, int rank, int mode, void* nccl_comm, void* const* pa
                  void* const* keys, void* const* flags, void* epoch, size_t part_elems, void** tp_out) {
   if (world < 1 || world > rb::kMaxRanks || rank < 0 || rank >= world)
     return rb::set_error("tp: world must be 1..8 and 0 <= rank < world");
-  if (mode != 1 && mode != 2) return rb::set_error("tp: mode 1 (NCCL) or 2 (peer memory)");
+  if (mode < 1 || mode > 3) return rb::set_error("tp: mode 1 (NCCL), 2 (peer memory) or 3 (GEMM push)");
   if (mode == 1 && world > 1 && !nccl_comm) return rb::set_error("tp: NCCL mode needs a communicator");
   if (!keys || !keys[rank]) return rb::set_error("tp: every rank needs an argmax key buffer");
-  if (mode == 2 && world > 1 && (!part0 || !part1 || !flags || !epoch))
+  if (mode >= 2 && world > 1 && (!part0 || !part1 || !flags || !epoch))
     return rb::set_error("tp: peer mode needs staging, flag and epoch buffers of every rank");
   rb::TpCtx* tp = new rb::TpCtx{};
   tp->world = world;
@@ -314,7 +394,7 @@ int rb_tp_create(int world, int rank, int mode, void* nccl_comm, void* const* pa
   tp->peers.rank = rank;
   for (int j = 0; j < world; ++j) {
     tp->peers.keys[j] = static_cast<unsigned long long*>(keys[j]);
-    if (mode == 2 && world > 1) {
+    if (mode >= 2 && world > 1) {
       tp->peers.part[0][j] = static_cast<__nv_bfloat16*>(part0[j]);
       tp->peers.part[1][j] = static_cast<__nv_bfloat16*>(part1[j]);
       tp->peers.flags[j] = static_cast<unsigned*>(flags[j]);

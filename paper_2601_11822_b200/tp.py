@@ -105,9 +105,10 @@ class _PhaseBuffers:
     """One rank's mode-2 buffers for one phase: two staging buffers [rows, H] bf16, argmax
     keys [rows] uint64, a zeroed flag array and zeroed per-CTA round counters."""
 
-    def __init__(self, rows: int, H: int, device):
+    def __init__(self, rows: int, H: int, device, slots: int = 1):
         words = ops.load().rb_tp_flag_words()
-        self.part = [torch.zeros(rows, H, dtype=torch.bfloat16, device=device) for _ in range(2)]
+        # mode 2: this rank's partial; mode 3: one receive slot per sender rank
+        self.part = [torch.zeros(slots * rows, H, dtype=torch.bfloat16, device=device) for _ in range(2)]
         self.keys = torch.zeros(rows, dtype=torch.int64, device=device)
         self.flags = torch.zeros(words, dtype=torch.int32, device=device)
         self.epoch = torch.zeros(AR_FLAG_SLOTS, dtype=torch.int32, device=device)
@@ -129,23 +130,26 @@ def _ipc_open(h, device) -> torch.Tensor:
 
 
 class IpcPeerGroup:
-    """Mode-2 contexts for one rank per process (the multi-GPU layout).
+    """Peer-memory contexts for one rank per process (the multi-GPU layout).
 
     Every rank allocates its buffers, exports cudaIpc handles through `pg` (a
-    torch.distributed group, gloo or NCCL) and maps its peers' buffers, so the one-shot
-    all-reduce kernel reads the peers' staging buffers and raises flags in their memory
-    directly (NVLink P2P across GPUs; the same device across processes in the tests)."""
+    torch.distributed group, gloo or NCCL) and maps its peers' buffers (NVLink P2P across
+    GPUs; the same device across processes in the tests). mode 2: the one-shot all-reduce
+    kernel reads the peers' staging buffers; mode 3: the row-parallel GEMM's epilogue pushes
+    its tiles into the peers' receive slots and the reduce reads only local memory."""
 
-    def __init__(self, runner, rank: int, world: int, pg=None, device="cuda"):
+    def __init__(self, runner, rank: int, world: int, pg=None, device="cuda", mode: int = 2):
         import torch.distributed as dist
 
+        if mode not in (2, 3):
+            raise ValueError("IpcPeerGroup: mode 2 (pull all-reduce) or 3 (GEMM push)")
         lib = ops.load()
         self.contexts: dict[str, TpContext] = {}
         self._keep = []
         for phase in ("pre", "dec"):
             buf = getattr(runner, phase)
             rows, H = buf.x.shape
-            mine = _PhaseBuffers(rows, H, device)
+            mine = _PhaseBuffers(rows, H, device, slots=world if mode == 3 else 1)
             handles = [None] * world
             dist.all_gather_object(handles, [_ipc_handle(t) for t in mine.shared()], group=pg)
             views = []
@@ -153,7 +157,7 @@ class IpcPeerGroup:
                 views.append(mine.shared() if j == rank else [_ipc_open(h, device) for h in handles[j]])
             ptr = [[v[k].data_ptr() for v in views] for k in range(4)]
             h = ctypes.c_void_p()
-            ops._check(lib.rb_tp_create(world, rank, 2, None, _vp_array(ptr[0]), _vp_array(ptr[1]),
+            ops._check(lib.rb_tp_create(world, rank, mode, None, _vp_array(ptr[0]), _vp_array(ptr[1]),
                                         _vp_array(ptr[2]), _vp_array(ptr[3]), mine.epoch.data_ptr(), rows * H,
                                         ctypes.byref(h)), "rb_tp_create")
             ctx = TpContext(h.value, [mine, views])

@@ -1,7 +1,7 @@
 """cfg 4 step times: Llama-3.1-70B (or any ARCHS model) tensor-parallel over the ranks of a
 torchrun job (one process per GPU), random-init shards of the real shapes.
 
-    torchrun --nproc-per-node 8 --master-addr 127.0.0.1 scripts/tp_step.py [--ar nccl|peer]
+    torchrun --nproc-per-node 8 --master-addr 127.0.0.1 scripts/tp_step.py [--ar nccl|peer|push]
              [--B 32,64,128] [--ctx 2560] [--T 2048]
     python scripts/tp_step.py            # world 1 (NCCL identity all-reduce)
 
@@ -27,7 +27,8 @@ from paper_2601_11822_b200.tp import IpcPeerGroup, NcclPhaseComms, local_arch, n
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--model", default="llama3.1-70b")
-    ap.add_argument("--ar", default="nccl", choices=["nccl", "peer"])
+    ap.add_argument("--ar", default="nccl", choices=["nccl", "peer", "push"],
+                    help="nccl | peer (one-shot pull all-reduce) | push (GEMM epilogue stores into every rank)")
     ap.add_argument("--B", default="32,64,128")
     ap.add_argument("--ctx", type=int, default=2560)
     ap.add_argument("--T", type=int, default=2048)
@@ -60,7 +61,7 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         NcclPhaseComms(r, rank, world, {"pre": obj[0][0], "dec": obj[0][1]})
     else:
-        IpcPeerGroup(r, rank, world)
+        IpcPeerGroup(r, rank, world, mode=2 if args.ar == "peer" else 3)
     sms = ops.device_sm_count(local)
     st = torch.cuda.Stream()
     toks = torch.randint(0, arch.vocab, (args.T,), dtype=torch.int32, device="cuda")

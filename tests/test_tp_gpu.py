@@ -48,7 +48,7 @@ def _prompt(vocab):
     return torch.randint(0, vocab, (P,), generator=torch.Generator().manual_seed(7), dtype=torch.int32)
 
 
-def _tp_rank(rank, world, port, out_dir):
+def _tp_rank(rank, world, port, out_dir, mode):
     import os
 
     import torch.distributed as dist
@@ -60,7 +60,7 @@ def _tp_rank(rank, world, port, out_dir):
     la = local_arch(arch, world)
     r = _runner(DecoderWeights.from_state(la, shard_state(arch, init_state(arch, seed=0), rank, world)),
                 vocab_offset=rank * la.vocab)
-    IpcPeerGroup(r, rank, world)
+    IpcPeerGroup(r, rank, world, mode=mode)
     prompt = _prompt(arch.vocab)
     logits = r.prefill(1, prompt[: P - 1].cuda(), 0, num_sms=148, logits=True).clone()
     r.last_tok[1] = int(prompt[P - 1])
@@ -75,7 +75,10 @@ def _tp_rank(rank, world, port, out_dir):
     dist.destroy_process_group()
 
 
-def test_tp2_ipc_peer_allreduce_matches_unsharded(tmp_path):
+@pytest.mark.parametrize("mode", [2, 3])
+def test_tp2_ipc_peer_allreduce_matches_unsharded(tmp_path, mode):
+    """mode 2: pull all-reduce kernel after the row-parallel GEMMs; mode 3: the GEMM epilogue
+    pushes its tiles into every rank's receive slot (GEMM and collective fused)."""
     import socket
 
     import torch.multiprocessing as mp
@@ -86,7 +89,7 @@ def test_tp2_ipc_peer_allreduce_matches_unsharded(tmp_path):
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
-    mp.spawn(_tp_rank, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_tp_rank, args=(world, port, str(tmp_path), mode), nprocs=world, join=True)
     res = [torch.load(tmp_path / f"rank{r}.pt") for r in range(world)]
     tp_logits = torch.cat([x["logits"][0] for x in res])
     full = _runner(DecoderWeights.from_state(arch, st))
