@@ -135,7 +135,8 @@ def run_reference(args, rank, world):
         "value": v, "unit": "output tokens/s", "n_gpus": world, "steps": len(vals), "warmup": 0,
         "ms_per_step": wall / len(vals) * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"cfg2 {args.model} in {PROMPT}/out {OUTPUT} (bounded CPU sample)"},
+        "config": {"workload": f"cfg3 {args.model} bf16 path restated in fp32 on the host, in {PROMPT}/out {OUTPUT} "
+                               f"(bounded CPU sample: one prefill chunk + one batched decode step)"},
         "cpu_baseline": {"value": v, "unit": "output tokens/s", "cores": vals[0]["cores"], "kind": "port",
                          "sample": vals[0]["sample"]},
         "e2e": {"value": v, "unit": "output tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

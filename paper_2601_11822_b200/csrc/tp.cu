@@ -421,6 +421,8 @@ int rb_tp_debug_nowait(void* tp, int on) {
  * its staging buffer of the current parity; NCCL mode: x holds this rank's contribution). */
 int rb_tp_allreduce(void* tp, void* x, long long n, void* stream) {
   rb::TpCtx* t = static_cast<rb::TpCtx*>(tp);
+  if (t && t->mode == 3 && t->world > 1)  // its inputs arrive only from a row-parallel GEMM's push epilogue
+    return rb::set_error("tp: mode 3 reduces only behind a pushing GEMM (rb_decoder_forward)");
   if (t && t->mode == 2 && t->world > 1) {
     // standalone use: stage x as this rank's partial and reduce into x (x = sum of partials)
     void* stage = t->peers.part[t->parity][t->rank];
