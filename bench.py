@@ -252,10 +252,10 @@ def main():
         args.arm = True  # one fused stream on the whole device; no split
         hchunk = int(args.engine.split("-", 1)[1])
         ex = HybridB200Executor(arch, seed=rank, max_batch=256, chunk_tokens=hchunk, max_context=PROMPT + OUTPUT + 64,
-                                num_slots=1024)
+                                num_slots=4096)
     else:
         ex = B200Executor(arch, seed=rank, static_decode_sms=None if args.arm else args.decode_sms, max_batch=256,
-                          chunk_tokens=2048, max_context=PROMPT + OUTPUT + 64, num_slots=1024)
+                          chunk_tokens=2048, max_context=PROMPT + OUTPUT + 64, num_slots=4096)
     policy = None
     if args.arm_profile and not hybrid:
         from paper_2601_11822_b200.arm import MeasuredArm, MeasuredProfile

@@ -178,7 +178,8 @@ class B200Executor:
         s = self._slot_of.get(req_id)
         if s is None:
             if not self._free_slots:
-                raise RuntimeError("out of request slots")
+                raise RuntimeError(f"out of request slots ({self.num_slots}): raise num_slots to cover the "
+                                   f"requests the KV pool can hold at once")
             s = self._free_slots.pop()
             self._slot_of[req_id] = s
         return s
