@@ -204,12 +204,16 @@ def main():
     ap.add_argument("--arm-policy", default="adaptive", choices=["balanced", "slo-min", "adaptive"])
     ap.add_argument("--arm", action="store_true",
                     help="the reference allocate() on the cost model instead of the measured ARM")
+    ap.add_argument("--arm-calibrated", default=None,
+                    help="with --arm: the reference cost model refitted to the B200 tables (profiler --calibrate JSON)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     PROMPT, OUTPUT = args.prompt, args.output
     SLO_ITL_US = int(args.slo_ms * 1e3)
     # default (cfg 3): RAPID with the measured adaptive ARM; --decode-sms N: cfg-2 static split;
     # --arm: the reference cost-model allocate()
+    if args.arm_calibrated:
+        args.arm = True
     if args.decode_sms is not None or args.arm or args.engine != "rapid":
         args.arm_profile = None
     elif args.arm_profile == "auto":
@@ -274,7 +278,17 @@ def main():
     if hybrid:
         engine = HybridEngine(model, b200_spec(), CostParams(), slo, chunk_tokens=hchunk, max_batch=256, executor=ex)
     else:
-        engine = RapidEngine(model, b200_spec(), CostParams(), slo, chunk_tokens=2048, max_batch=256, executor=ex,
+        gpu_spec, cost_params = b200_spec(), CostParams()
+        if args.arm_calibrated:  # the reference allocate() on the refitted model
+            import dataclasses
+
+            from paper_2601_11822_b200.specs import GpuSpec
+
+            with open(args.arm_calibrated) as fh:
+                fit = json.load(fh)
+            gpu_spec = GpuSpec(**fit["gpu"])
+            cost_params = dataclasses.replace(CostParams(), **fit["params"])
+        engine = RapidEngine(model, gpu_spec, cost_params, slo, chunk_tokens=2048, max_batch=256, executor=ex,
                              static_decision=None if args.arm else static, record_decisions=args.arm,
                              arm_policy=policy)
 

@@ -11,6 +11,7 @@ chunk time under that load is recorded too, so a policy can trade decode
 latency against prefill throughput.
 
     python -m paper_2601_11822_b200.profiler --model llama3.1-8b --ctx 1152 --out profiles/arm_llama8b.json
+    python -m paper_2601_11822_b200.profiler --calibrate profiles/arm/<profile>.json --model llama3.1-8b --out fit.json
 
 The JSON holds {"decode_us": {D: {B: us}}, "overalloc_decode_us": {B: us},
 "prefill_us_per_token": {D: us}, "prefill_us_per_token_by_batch": {D: {B: us}}, ...};
@@ -143,8 +144,25 @@ def measure(model: str = "llama3.1-8b", ctx: int = 1152, chunk: int = 2048, ladd
     return out
 
 
+def calibrate_file(profile_path: str, model: str, out: str) -> dict:
+    """Refit the reference cost model (GpuSpec / CostParams) to a measured profile."""
+    import dataclasses
+
+    from paper_2601_11822_b200.arm import CostParams, MeasuredProfile, calibrate
+    from paper_2601_11822_b200.specs import b200_spec
+
+    res = calibrate(MeasuredProfile.load(profile_path), ARCHS[model].model_spec(), b200_spec(), CostParams())
+    res["profile"] = profile_path
+    res["model"] = model
+    with open(out, "w") as fh:
+        json.dump(res, fh, indent=1, default=lambda o: dataclasses.asdict(o) if dataclasses.is_dataclass(o) else o)
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--calibrate", default=None,
+                    help="refit the reference cost model to this measured profile (no GPU needed); writes --out")
     ap.add_argument("--model", default="llama3.1-8b")
     ap.add_argument("--ctx", type=int, default=1152)
     ap.add_argument("--chunk", type=int, default=2048)
@@ -152,6 +170,10 @@ def main():
     ap.add_argument("--batches", default=",".join(map(str, DEFAULT_BATCH_GRID)))
     ap.add_argument("--out", required=True)
     args = ap.parse_args()
+    if args.calibrate:
+        r = calibrate_file(args.calibrate, args.model, args.out)
+        print(json.dumps({k: r[k] for k in ("fit", "partition_decode_rel_err", "overallocate_decode_rel_err")}))
+        return
     res = measure(args.model, args.ctx, args.chunk, tuple(int(x) for x in args.ladder.split(",")),
                   tuple(int(x) for x in args.batches.split(",")))
     with open(args.out, "w") as fh:

@@ -131,3 +131,44 @@ def test_committed_b200_profiles(name):
                 assert mp.decode_us(d, b) <= arm.target
     lines = profile_lines(mp.to_profile(50_000))
     assert len(lines) == len(mp.batches)
+
+
+def test_calibrate_recovers_cost_model_parameters():
+    """Tables generated by the reference decode_time itself (known bandwidth factor, plateau
+    and overhead) are fitted back by arm.calibrate with ~zero error."""
+    import dataclasses
+
+    from paper_2601_11822_b200.arm import CostParams, calibrate, decode_time, prefill_time
+    from paper_2601_11822_b200.specs import ARCHS, b200_spec
+
+    model = ARCHS["llama3.1-8b"].model_spec()
+    gpu0 = b200_spec()
+    g = dataclasses.replace(gpu0, hbm_bandwidth=gpu0.hbm_bandwidth * 0.8, peak_flops=gpu0.peak_flops * 0.9)
+    p = dataclasses.replace(CostParams(), decode_plateau_fraction=0.5, fixed_iteration_overhead_us=1000.0)
+    ctx, chunk = 1152, 1024
+    dec = {str(d): {str(b): float(decode_time(b, b * ctx, d / 148, model, g, p, concurrent=True))
+                    for b in DEFAULT_BATCH_GRID} for d in LADDER}
+    pre = {str(d): prefill_time(chunk, (148 - d) / 148, model, g, p, concurrent=True) / chunk for d in LADDER}
+    mp = MeasuredProfile({"model": "x", "ctx": ctx, "chunk": chunk, "total_sms": 148, "granularity": 8,
+                          "batches": list(DEFAULT_BATCH_GRID), "decode_us": dec, "prefill_us_per_token": pre,
+                          "overalloc_decode_us": {str(b): 30_000.0 for b in DEFAULT_BATCH_GRID},
+                          "overalloc_prefill_us_per_token": 15.0})
+    res = calibrate(mp, model, gpu0, CostParams())
+    assert abs(res["fit"]["hbm_bandwidth_factor"] - 0.8) < 1e-9
+    assert abs(res["fit"]["decode_plateau_fraction"] - 0.5) < 1e-9
+    assert res["fit"]["fixed_iteration_overhead_us"] == 1000.0
+    assert abs(res["fit"]["peak_flops_factor"] - 0.9) < 0.03
+    assert res["partition_decode_rel_err"]["max"] < 1e-3
+
+
+def test_committed_cost_fits():
+    """The refits written from the measured tables: partition decode steps within a few % (median),
+    and the reference OVERALLOCATE model far below the measured contended steps."""
+    import json
+    import os
+
+    for name in ("llama3.1-8b_costfit.json", "qwen2.5-14b_costfit.json"):
+        with open(os.path.join(os.path.dirname(os.path.dirname(__file__)), "profiles", "arm", name)) as fh:
+            fit = json.load(fh)
+        assert fit["partition_decode_rel_err"]["median"] < 0.1
+        assert fit["overallocate_decode_rel_err"]["median"] < -0.3
