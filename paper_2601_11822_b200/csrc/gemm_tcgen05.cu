@@ -39,9 +39,14 @@ constexpr int kBK = 64;                 // bf16 elements per 128-byte swizzle ro
 constexpr int kABytes = kBM * kBK * 2;  // 16 KB
 // Epilogue warp sets (template kSets): each TMEM quadrant is drained by kSets warps taking
 // alternate 32-column chunks. Decode (swap-AB) GEMMs are short and their split-tile epilogue
-// is on the critical path: 2 sets (320 threads, 168 registers); prefill GEMMs overlap the
-// epilogue with the next tile's MMAs: 1 set (192 threads, no register cap).
-constexpr int threads_for(int sets) { return 64 + 128 * sets; }
+// is on the critical path: 2 sets; prefill GEMMs overlap the epilogue with the next tile's
+// MMAs: 1 set (192 threads: producer, MMA, 4 epilogue warps; no register cap).
+// The 2-set kernel runs 384 threads as three warpgroups: WG0 = producer, MMA issuer and two
+// idle warps, which give their registers back (setmaxnreg.dec 56) so the epilogue warpgroups
+// WG1/WG2 run at 224 registers instead of the 168 a flat 384-thread launch allows (the flat
+// 320-thread layout spilled ~210 bytes per thread in the split-tile accumulate).
+constexpr int threads_for(int sets) { return sets == 2 ? 384 : 64 + 128 * sets; }
+constexpr int epi_first_warp(int sets) { return sets == 2 ? 4 : 2; }
 constexpr int kMaxEpiWarps = 8;
 constexpr int kStgStride = 40;          // bf16 per staging row (32 + 8 pad, 80 B)
 constexpr int kStgBytes = 32 * kStgStride * 2;  // per epilogue warp
@@ -463,139 +468,149 @@ __global__ void __launch_bounds__(threads_for(kSets), 1)
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
   if (threadIdx.x == 0) TRACE(1);
   pdl_trigger();  // the next kernel may start its prologue as our CTAs drain
-  if (warp == 0) {
-    // Weights do not depend on the preceding kernel: warm L2 with this CTA's first
-    // k-blocks of them while that kernel finishes, then wait for its outputs.
-    SegIter s0(g, cid, ncl);
-    int t, kb0, kb1;
-    if (s0.next(g, t, kb0, kb1)) {
-      const int mt = t % g.m_tiles;
-      const int nt = t / g.m_tiles;
-      const int kend = min(kb1, kb0 + stages);
-      for (int kb = kb0; kb < kend; ++kb) {
-        if (g.swap) {
-          const int r0 = mt * tile_rows + (int)rank * kBM;
+  // setmaxnreg sits at the top of each warpgroup's branch: ptxas allocates the code below it
+  // with that budget (code reachable from both would get the smaller one)
+  if (warp < epi_first_warp(kSets)) {
+    if constexpr (kSets == 2) {
+      // 384 x 168 at launch; WG0 hands 128 x 112 registers to the two epilogue warpgroups
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+    }
+    if (warp == 0) {
+      // Weights do not depend on the preceding kernel: warm L2 with this CTA's first
+      // k-blocks of them while that kernel finishes, then wait for its outputs.
+      SegIter s0(g, cid, ncl);
+      int t, kb0, kb1;
+      if (s0.next(g, t, kb0, kb1)) {
+        const int mt = t % g.m_tiles;
+        const int nt = t / g.m_tiles;
+        const int kend = min(kb1, kb0 + stages);
+        for (int kb = kb0; kb < kend; ++kb) {
+          if (g.swap) {
+            const int r0 = mt * tile_rows + (int)rank * kBM;
 #pragma unroll
-          for (int i = 0; i < kMT; ++i) {
-            const int r = r0 + i * kBM * kPair;
-            if (g.a_blocked) tma_prefetch_l2_2d_w(&tmap_a, 0, ((r / kBM) * g.num_kb + kb) * kBM);
-            else tma_prefetch_l2_2d_w(&tmap_a, kb * kBK, r);
+            for (int i = 0; i < kMT; ++i) {
+              const int r = r0 + i * kBM * kPair;
+              if (g.a_blocked) tma_prefetch_l2_2d_w(&tmap_a, 0, ((r / kBM) * g.num_kb + kb) * kBM);
+              else tma_prefetch_l2_2d_w(&tmap_a, kb * kBK, r);
+            }
+          } else {
+            tma_prefetch_l2_2d_w(&tmap_b, kb * kBK, nt * BN + (int)rank * bn_cta);
           }
-        } else {
-          tma_prefetch_l2_2d_w(&tmap_b, kb * kBK, nt * BN + (int)rank * bn_cta);
         }
       }
     }
-  }
-  pdl_wait();
+    pdl_wait();
 
-  if (warp == 0) {
-    // ================= TMA producer (both CTAs; whole warp, one elected lane issues) =================
-    const uint32_t full_leader0 = (kPair == 2) ? mapa_shared(&full[0], 0) : 0u;
-    int stage = 0;
-    uint32_t phase = 0;
-    SegIter seg(g, cid, ncl);
-    int t, kb0, kb1;
-    while (seg.next(g, t, kb0, kb1)) {
-      const int mt = t % g.m_tiles;
-      const int nt = t / g.m_tiles;
-      const int arow = mt * tile_rows + (int)rank * kBM;
-      const int brow = nt * BN + (int)rank * bn_cta;
-      // blocked A: 128-row block r, k-block kb lives at rows (r * num_kb + kb) * 128, column 0
-      auto a_x = [&](int kb) { return g.a_blocked ? 0 : kb * kBK; };
-      auto a_y = [&](int kb, int i) {
-        const int r = arow + i * kBM * kPair;
-        return g.a_blocked ? ((r / kBM) * g.num_kb + kb) * kBM : r;
-      };
-      if (g.pf_dist > 0) {
-        for (int kb = kb0; kb < min(kb1, kb0 + g.pf_dist); ++kb)
-#pragma unroll
-          for (int i = 0; i < kMT; ++i) tma_prefetch_l2_2d_w(&tmap_a, a_x(kb), a_y(kb, i));
-      }
-      for (int kb = kb0; kb < kb1; ++kb) {
-        if (g.pf_dist > 0 && kb + g.pf_dist < kb1) {
-#pragma unroll
-          for (int i = 0; i < kMT; ++i) tma_prefetch_l2_2d_w(&tmap_a, a_x(kb + g.pf_dist), a_y(kb + g.pf_dist, i));
-        }
-        mbar_wait(&empty[stage], phase ^ 1);
-        uint8_t* a_dst = sA + (size_t)stage * a_bytes;
-        if (kPair == 1 && (g.dbg & 2)) {
-          mbar_arrive_w(&full[stage]);
-        } else if (kPair == 2) {
-          const uint32_t lbar = full_leader0 + (uint32_t)stage * 8u;
-          if (leader) mbar_arrive_expect_tx_w(&full[stage], kPair * (a_bytes + b_bytes));
-#pragma unroll
-          for (int i = 0; i < kMT; ++i)
-            tma_load_2d_pair_w(a_dst + (size_t)i * kABytes, &tmap_a, lbar, a_x(kb), a_y(kb, i), g.hint_a);
-          tma_load_2d_pair_w(sB + (size_t)stage * b_bytes, &tmap_b, lbar, kb * kBK, brow, g.hint_b);
-        } else {
-          mbar_arrive_expect_tx_w(&full[stage], a_bytes + b_bytes);
-#pragma unroll
-          for (int i = 0; i < kMT; ++i)
-            tma_load_2d_w(a_dst + (size_t)i * kABytes, &tmap_a, &full[stage], a_x(kb), a_y(kb, i), g.hint_a);
-          tma_load_2d_w(sB + (size_t)stage * b_bytes, &tmap_b, &full[stage], kb * kBK, brow, g.hint_b);
-        }
-        if (++stage == stages) { stage = 0; phase ^= 1; }
-      }
-    }
-  } else if (warp == 1) {
-    if (leader) {
-      // ================= MMA issuer (leader CTA; whole warp, one elected lane issues) =================
-      const uint32_t idesc = make_idesc_bf16(kBM * kPair, BN);
-      const uint32_t ka_mask = (uint32_t)KA - 1u;
+    if (warp == 0) {
+      // ================= TMA producer (both CTAs; whole warp, one elected lane issues) =================
+      const uint32_t full_leader0 = (kPair == 2) ? mapa_shared(&full[0], 0) : 0u;
       int stage = 0;
       uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      bool first = true;
       SegIter seg(g, cid, ncl);
       int t, kb0, kb1;
       while (seg.next(g, t, kb0, kb1)) {
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + (uint32_t)acc * acc_stride;
+        const int mt = t % g.m_tiles;
+        const int nt = t / g.m_tiles;
+        const int arow = mt * tile_rows + (int)rank * kBM;
+        const int brow = nt * BN + (int)rank * bn_cta;
+        // blocked A: 128-row block r, k-block kb lives at rows (r * num_kb + kb) * 128, column 0
+        auto a_x = [&](int kb) { return g.a_blocked ? 0 : kb * kBK; };
+        auto a_y = [&](int kb, int i) {
+          const int r = arow + i * kBM * kPair;
+          return g.a_blocked ? ((r / kBM) * g.num_kb + kb) * kBM : r;
+        };
+        if (g.pf_dist > 0) {
+          for (int kb = kb0; kb < min(kb1, kb0 + g.pf_dist); ++kb)
+#pragma unroll
+            for (int i = 0; i < kMT; ++i) tma_prefetch_l2_2d_w(&tmap_a, a_x(kb), a_y(kb, i));
+        }
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&full[stage], phase);
-          if (lane == 0 && first && kb == kb0) TRACE(2);
-          if (lane == 0 && first && kb == kb1 - 1) TRACE(3);
-          tc_fence_after();
-          if (kPair == 1 && (g.dbg & 1)) {
-            mbar_arrive_w(&empty[stage]);
+          if (g.pf_dist > 0 && kb + g.pf_dist < kb1) {
+#pragma unroll
+            for (int i = 0; i < kMT; ++i) tma_prefetch_l2_2d_w(&tmap_a, a_x(kb + g.pf_dist), a_y(kb + g.pf_dist, i));
+          }
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* a_dst = sA + (size_t)stage * a_bytes;
+          if (kPair == 1 && (g.dbg & 2)) {
+            mbar_arrive_w(&full[stage]);
+          } else if (kPair == 2) {
+            const uint32_t lbar = full_leader0 + (uint32_t)stage * 8u;
+            if (leader) mbar_arrive_expect_tx_w(&full[stage], kPair * (a_bytes + b_bytes));
+#pragma unroll
+            for (int i = 0; i < kMT; ++i)
+              tma_load_2d_pair_w(a_dst + (size_t)i * kABytes, &tmap_a, lbar, a_x(kb), a_y(kb, i), g.hint_a);
+            tma_load_2d_pair_w(sB + (size_t)stage * b_bytes, &tmap_b, lbar, kb * kBK, brow, g.hint_b);
           } else {
-            const uint64_t bdesc = make_sdesc_sw128(sB + (size_t)stage * b_bytes);
-            const uint64_t adesc0 = make_sdesc_sw128(sA + (size_t)stage * a_bytes);
-            // kk outer, sub-tile inner: consecutive MMAs hit different accumulators
+            mbar_arrive_expect_tx_w(&full[stage], a_bytes + b_bytes);
 #pragma unroll
-            for (int kk = 0; kk < kBK / 16; ++kk) {
-              // advance 16 elements (32 bytes) inside the swizzle atom: +2 in 16-byte units
-              const uint32_t j = (uint32_t)kk & ka_mask;
-              const uint32_t accum = (kb > kb0 || (uint32_t)kk > ka_mask) ? 1u : 0u;
-#pragma unroll
-              for (int i = 0; i < kMT; ++i) {
-                const uint64_t adesc = adesc0 + (uint64_t)((i * kABytes) >> 4) + (uint64_t)(kk * 2);
-                const uint32_t d = d_tmem + j * sub_stride + (uint32_t)(i * BN);
-                if (kPair == 2) umma_bf16_pair_w(d, adesc, bdesc + (uint64_t)(kk * 2), idesc, accum);
-                else umma_bf16_w(d, adesc, bdesc + (uint64_t)(kk * 2), idesc, accum);
-              }
-            }
-            if (kPair == 2) umma_commit_pair_mc_w(&empty[stage], 0x3);
-            else umma_commit_w(&empty[stage]);
+            for (int i = 0; i < kMT; ++i)
+              tma_load_2d_w(a_dst + (size_t)i * kABytes, &tmap_a, &full[stage], a_x(kb), a_y(kb, i), g.hint_a);
+            tma_load_2d_w(sB + (size_t)stage * b_bytes, &tmap_b, &full[stage], kb * kBK, brow, g.hint_b);
           }
           if (++stage == stages) { stage = 0; phase ^= 1; }
         }
-        if (kPair == 2) umma_commit_pair_mc_w(&tfull[acc], 0x3);
-        else if (g.dbg & 1) mbar_arrive_w(&tfull[acc]);
-        else umma_commit_w(&tfull[acc]);
-        if (++acc == g.nacc) { acc = 0; acc_phase ^= 1; }
-        first = false;
+      }
+    } else if (warp == 1) {
+      if (leader) {
+        // ================= MMA issuer (leader CTA; whole warp, one elected lane issues) =================
+        const uint32_t idesc = make_idesc_bf16(kBM * kPair, BN);
+        const uint32_t ka_mask = (uint32_t)KA - 1u;
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        bool first = true;
+        SegIter seg(g, cid, ncl);
+        int t, kb0, kb1;
+        while (seg.next(g, t, kb0, kb1)) {
+          mbar_wait(&tempty[acc], acc_phase ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + (uint32_t)acc * acc_stride;
+          for (int kb = kb0; kb < kb1; ++kb) {
+            mbar_wait(&full[stage], phase);
+            if (lane == 0 && first && kb == kb0) TRACE(2);
+            if (lane == 0 && first && kb == kb1 - 1) TRACE(3);
+            tc_fence_after();
+            if (kPair == 1 && (g.dbg & 1)) {
+              mbar_arrive_w(&empty[stage]);
+            } else {
+              const uint64_t bdesc = make_sdesc_sw128(sB + (size_t)stage * b_bytes);
+              const uint64_t adesc0 = make_sdesc_sw128(sA + (size_t)stage * a_bytes);
+              // kk outer, sub-tile inner: consecutive MMAs hit different accumulators
+#pragma unroll
+              for (int kk = 0; kk < kBK / 16; ++kk) {
+                // advance 16 elements (32 bytes) inside the swizzle atom: +2 in 16-byte units
+                const uint32_t j = (uint32_t)kk & ka_mask;
+                const uint32_t accum = (kb > kb0 || (uint32_t)kk > ka_mask) ? 1u : 0u;
+#pragma unroll
+                for (int i = 0; i < kMT; ++i) {
+                  const uint64_t adesc = adesc0 + (uint64_t)((i * kABytes) >> 4) + (uint64_t)(kk * 2);
+                  const uint32_t d = d_tmem + j * sub_stride + (uint32_t)(i * BN);
+                  if (kPair == 2) umma_bf16_pair_w(d, adesc, bdesc + (uint64_t)(kk * 2), idesc, accum);
+                  else umma_bf16_w(d, adesc, bdesc + (uint64_t)(kk * 2), idesc, accum);
+                }
+              }
+              if (kPair == 2) umma_commit_pair_mc_w(&empty[stage], 0x3);
+              else umma_commit_w(&empty[stage]);
+            }
+            if (++stage == stages) { stage = 0; phase ^= 1; }
+          }
+          if (kPair == 2) umma_commit_pair_mc_w(&tfull[acc], 0x3);
+          else if (g.dbg & 1) mbar_arrive_w(&tfull[acc]);
+          else umma_commit_w(&tfull[acc]);
+          if (++acc == g.nacc) { acc = 0; acc_phase ^= 1; }
+          first = false;
+        }
       }
     }
   } else {
-    // ================= epilogue warps 2.. (both CTAs) =================
+    if constexpr (kSets == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
+    pdl_wait();
+    // ================= epilogue warps (both CTAs) =================
     // warp w may only read TMEM lane quadrant w % 4; the kEpiSets warps of a quadrant take
     // alternate 32-column chunks of every accumulator (the epilogue is latency-bound per warp)
     const int q = warp & 3;
-    const int ew = warp - 2;
+    const int ew = warp - epi_first_warp(kSets);
     const int set = ew >> 2;
     const bool lead = lane == 0 && q == 0 && set == 0;  // one thread of the CTA's epilogue
     __nv_bfloat16* stg = stg_all + (size_t)ew * (kStgBytes / 2);
