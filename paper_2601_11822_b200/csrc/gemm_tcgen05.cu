@@ -789,6 +789,7 @@ int gemm_set_pair_mode(int mode) {
 // debug override of the decode (swap-AB) schedule: -1 auto; else bit0 = 2 A sub-tiles
 // per tile, bit1 = stream-K (without it: data-parallel whole tiles)
 static int g_force_variant = -1;
+static int g_mt2_sets = 1;  // debug: epilogue sets of the two-sub-tile (MT=2) decode kernel
 static int g_prefill_streamk = 0;          // stream-K for badly wave-quantized token-major GEMMs
 static double g_prefill_streamk_frac = 0.6;
 int gemm_set_prefill_streamk(int on, double max_frac) {
@@ -798,6 +799,7 @@ int gemm_set_prefill_streamk(int on, double max_frac) {
 }
 int gemm_set_variant(int v) {
   g_force_variant = v;
+  g_mt2_sets = (v >= 0 && (v & (1 << 14))) ? 2 : 1;
   return 0;
 }
 
@@ -850,7 +852,15 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
   // (variant bit 0) measured slower once the MMA issue loop was lean: off by default.
   int variant = swap ? 2 : 0;
   if (g_force_variant >= 0) variant = swap ? g_force_variant : (g_force_variant & ~1);
-  int MT = ((variant & 1) && 4 * BN <= 512 && M > kBM * pair) ? 2 : 1;
+  int MT = ((variant & 1) && 2 * BN <= 512 && M > kBM * pair) ? 2 : 1;
+  // Small decode batches: two A sub-tiles per stage (36 KB stages, half the stages and
+  // barrier round trips per weight byte) measured 9-26% faster at B <= 32 and on the large
+  // projections at B <= 64 on decode partitions up to ~88 SMs (per-SM ingest bound; see
+  // scripts/gemm_chain.py); on the whole GPU (HBM bound) the extra split-tile fixups of the
+  // halved tile count cost 2-15%, and the wider epilogue loses above B = 64.
+  if (swap && g_force_variant < 0 && M > kBM * pair && num_sms <= 88 &&
+      (BN <= 32 || (BN <= 64 && (long long)M * K >= (32ll << 20))))
+    MT = 2;
   const int bn_cta = BN / pair;
   const int a_bytes = MT * kABytes;
   const int stage_bytes = a_bytes + bn_cta * kBK * 2;
@@ -940,11 +950,12 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
   // [pair][MT][sets]: decode (swap-AB) with single A sub-tiles uses 2 epilogue sets
   static const KernelFn kernels[2][2][2] = {
       {{gemm_bf16_tcgen05_kernel<1, 1, 1>, gemm_bf16_tcgen05_kernel<1, 1, 2>},
-       {gemm_bf16_tcgen05_kernel<1, 2, 1>, gemm_bf16_tcgen05_kernel<1, 2, 1>}},
+       {gemm_bf16_tcgen05_kernel<1, 2, 1>, gemm_bf16_tcgen05_kernel<1, 2, 2>}},
       {{gemm_bf16_tcgen05_kernel<2, 1, 1>, gemm_bf16_tcgen05_kernel<2, 1, 2>},
-       {gemm_bf16_tcgen05_kernel<2, 2, 1>, gemm_bf16_tcgen05_kernel<2, 2, 1>}}};
+       {gemm_bf16_tcgen05_kernel<2, 2, 1>, gemm_bf16_tcgen05_kernel<2, 2, 2>}}};
   static bool attr_done[2][2][2] = {};
-  const int sets = (swap && MT == 1) ? 2 : 1;
+  // decode epilogue sets: 2 (three warpgroups, setmaxnreg) except the MT=2 kernel at B <= 32
+  const int sets = (swap && (MT == 1 || g_mt2_sets == 2 || (g_force_variant < 0 && BN > 32))) ? 2 : 1;
   const KernelFn kern = kernels[pair - 1][MT - 1][sets - 1];
   if (!attr_done[pair - 1][MT - 1][sets - 1]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);

@@ -50,9 +50,11 @@ def main():
     ap.add_argument("--n", type=int, default=8)
     ap.add_argument("--shapes", default="qkv,o,gate_up,down")
     ap.add_argument("--variant", type=int, default=-1)
+    ap.add_argument("--pair", type=int, default=-1, help="-1 auto, 0 single CTA, 1 CTA pair")
     args = ap.parse_args()
     lib = ops.load()
     lib.rb_debug_gemm_variant(args.variant)
+    lib.rb_debug_gemm_pair_mode(args.pair)
     if args.sms >= 148:
         st, sms = torch.cuda.Stream(), 148
     else:

@@ -53,7 +53,7 @@ def test_linear_bias_residual(scratch):
 
 
 @pytest.mark.parametrize("T", [1, 7, 16, 33, 64, 128, 200, 256])
-@pytest.mark.parametrize("O,K", [(4096, 4096), (6144, 4096), (1024, 14336)])
+@pytest.mark.parametrize("O,K", [(4096, 4096), (6144, 4096), (1024, 14336), (8192, 4096)])
 def test_linear_swap_ab(T, O, K, scratch):
     g = torch.Generator(device=DEV).manual_seed(T * 31 + O)
     x = torch.randn(T, K, device=DEV, generator=g).bfloat16()
@@ -62,10 +62,13 @@ def test_linear_swap_ab(T, O, K, scratch):
     r = torch.randn(T, O, device=DEV, generator=g).bfloat16()
     y = ops.linear(x, w, bias=b, residual=r, mode=2, scratch=scratch)
     y2 = ops.linear(x, w, bias=b, residual=r, mode=2, scratch=None)  # no split-K
+    # a decode-partition grid: two A sub-tiles per stage at small batches (MT=2 kernels)
+    y3 = ops.linear(x, w, bias=b, residual=r, mode=2, scratch=scratch, num_sms=64)
     torch.cuda.synchronize()
     ref = x.float() @ w.float().T + b.float() + r.float()
     assert rel_l2(y, ref) < 1e-2
     assert rel_l2(y2, ref) < 1e-2
+    assert rel_l2(y3, ref) < 1e-2
 
 
 @pytest.mark.parametrize("T,mode", [(1, 2), (37, 2), (200, 2), (300, 1), (1023, 1)])
@@ -283,7 +286,8 @@ def test_rope_cache_write():
         assert torch.equal(cache[page, 1, :, p % 16], v)
 
 
-@pytest.mark.parametrize("T,mode,bias,sms", [(7, 2, False, 148), (128, 2, True, 72), (200, 0, False, 148),
+@pytest.mark.parametrize("T,mode,bias,sms", [(7, 2, False, 148), (24, 2, True, 64), (128, 2, True, 72),
+                                             (200, 0, False, 148),
                                              (777, 1, True, 76), (1023, 1, False, 148)])
 def test_qkv_rope_fused(T, mode, bias, sms, scratch):
     """rb_gemm_qkv_rope (QKV GEMM with RoPE + paged K/V write in its epilogue) against
