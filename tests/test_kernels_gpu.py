@@ -71,9 +71,10 @@ def test_linear_swap_ab(T, O, K, scratch):
     assert rel_l2(y3, ref) < 1e-2
 
 
-@pytest.mark.parametrize("T,mode", [(1, 2), (37, 2), (200, 2), (300, 1), (1023, 1)])
+@pytest.mark.parametrize("T,mode,sms", [(1, 2, 148), (1, 2, 64), (37, 2, 148), (37, 2, 64), (200, 2, 148),
+                                        (300, 1, 148), (1023, 1, 148)])
 @pytest.mark.parametrize("I", [1024, 3584])
-def test_linear_fused_swiglu(T, mode, I, scratch):
+def test_linear_fused_swiglu(T, mode, sms, I, scratch):
     """mode | 4: gate/up rows interleaved in 16-blocks, epilogue emits silu(gate) * up."""
     from paper_2601_11822_b200.model import interleave_gate_up
 
@@ -84,7 +85,7 @@ def test_linear_fused_swiglu(T, mode, I, scratch):
     up = (torch.randn(I, K, device=DEV, generator=g) * 0.05).bfloat16()
     w = interleave_gate_up(gate, up).contiguous()
     y = torch.empty(T, I, device=DEV, dtype=torch.bfloat16)
-    ops.load().rb_gemm_bf16(x.data_ptr(), w.data_ptr(), y.data_ptr(), None, None, T, 2 * I, K, K, K, I, mode | 4, 148,
+    ops.load().rb_gemm_bf16(x.data_ptr(), w.data_ptr(), y.data_ptr(), None, None, T, 2 * I, K, K, K, I, mode | 4, sms,
                             scratch.ws.data_ptr(), scratch.ws_bytes, scratch.counters.data_ptr(),
                             scratch.counters.numel(), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
