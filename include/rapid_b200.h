@@ -41,6 +41,9 @@ int rb_debug_gemm_variant(int v);
 /* Debug: stream-K for token-major (prefill) GEMMs whose whole-tile waves quantize badly
  * (fewer than 4 waves, last wave at most max_frac full); default off (measured slower). */
 int rb_debug_gemm_prefill_streamk(int on, double max_frac);
+/* Debug: token-major (prefill) GEMM tile width; 0 = wave-aware choice (default), else a forced
+ * multiple of 32 in [32, 256]. Returns -1 for an invalid width. */
+int rb_debug_gemm_prefill_bn(int bn);
 /* Programmatic dependent launch for the forward's kernels (default on): each kernel may
  * start its prologue while its predecessor in the stream drains. 0 = plain serialization. */
 int rb_set_pdl(int on);

@@ -31,6 +31,7 @@ int gemm_set_trace(unsigned long long* buf);
 int gemm_set_pair_mode(int mode);
 int gemm_set_variant(int v);
 int gemm_set_prefill_streamk(int on, double max_frac);
+int gemm_set_prefill_bn(int bn);
 }  // namespace rb
 
 #define ST(s) reinterpret_cast<cudaStream_t>(s)
@@ -44,6 +45,7 @@ int rb_debug_gemm_trace(unsigned long long* buf) { return rb::gemm_set_trace(buf
 int rb_debug_gemm_pair_mode(int mode) { return rb::gemm_set_pair_mode(mode); }
 int rb_debug_gemm_variant(int v) { return rb::gemm_set_variant(v); }
 int rb_debug_gemm_prefill_streamk(int on, double max_frac) { return rb::gemm_set_prefill_streamk(on, max_frac); }
+int rb_debug_gemm_prefill_bn(int bn) { return rb::gemm_set_prefill_bn(bn); }
 int rb_set_pdl(int on) {
   rb::set_pdl(on != 0);
   return 0;

@@ -790,6 +790,12 @@ int gemm_set_pair_mode(int mode) {
 // per tile, bit1 = stream-K (without it: data-parallel whole tiles)
 static int g_force_variant = -1;
 static int g_mt2_sets = 1;  // debug: epilogue sets of the two-sub-tile (MT=2) decode kernel
+static int g_prefill_bn = 0;  // token-major tile width: 0 = wave-aware choice, else forced (debug)
+int gemm_set_prefill_bn(int bn) {
+  if (bn != 0 && (bn < 32 || bn > 256 || bn % 32 != 0)) return -1;
+  g_prefill_bn = bn;
+  return 0;
+}
 static int g_prefill_streamk = 0;          // stream-K for badly wave-quantized token-major GEMMs
 static double g_prefill_streamk_frac = 0.6;
 int gemm_set_prefill_streamk(int on, double max_frac) {
@@ -839,7 +845,26 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
     BN = ((N + 31) / 32) * 32;
     if (BN > 256) BN = 256;
   } else {
+    // Token-major (prefill) tiles are 256 x BN on CTA pairs. Whole-tile waves quantize: the
+    // O / down projections of a 1K-token chunk are 4 x 16 tiles of 256 columns, 1.5 waves on a
+    // 42-pair partition, run as 2. Pick the width (multiple of 32, >= 128) that minimises
+    // waves x (BN + per-tile overhead): 224 there (2 waves of narrower tiles).
     BN = 256;
+    if (g_prefill_bn) {
+      BN = g_prefill_bn;
+    } else if (T > kBM) {
+      const long long slots = num_sms >= 2 ? num_sms / 2 : 1;
+      const long long mt = (T + 2 * kBM - 1) / (2 * kBM);
+      long long best = -1;
+      for (int bn = 256; bn >= 128; bn -= 32) {
+        const long long tiles = mt * ((N + bn - 1) / bn);
+        const long long cost = ((tiles + slots - 1) / slots) * (bn + 32);
+        if (best < 0 || cost < best) {
+          best = cost;
+          BN = bn;
+        }
+      }
+    }
   }
   // CTA pairs halve the per-SM operand stream: prefill tiles always; decode (swap-AB)
   // tiles when the batch tile is wide (each CTA of the pair stages BN/2 activation rows,

@@ -32,6 +32,7 @@ _SIGS = {
     "rb_debug_gemm_pair_mode": ([_c_int], _c_int),
     "rb_debug_gemm_variant": ([_c_int], _c_int),
     "rb_debug_gemm_prefill_streamk": ([_c_int, ctypes.c_double], _c_int),
+    "rb_debug_gemm_prefill_bn": ([_c_int], _c_int),
     "rb_set_pdl": ([_c_int], _c_int),
     "rb_set_decode_glu": ([_c_int], _c_int),
     "rb_gemm_bf16": (

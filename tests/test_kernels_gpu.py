@@ -71,6 +71,45 @@ def test_linear_swap_ab(T, O, K, scratch):
     assert rel_l2(y3, ref) < 1e-2
 
 
+@pytest.mark.parametrize("bn", [0, 128, 160, 192, 224, 256])
+def test_linear_prefill_tile_widths(bn, scratch):
+    """Token-major GEMM at every tile width the wave-aware chooser can pick (0 = its own choice
+    on an 84-SM grid: 224 for a 1023-token O projection), plain + bias/residual and SwiGLU."""
+    from paper_2601_11822_b200.model import interleave_gate_up
+
+    lib = ops.load()
+    assert lib.rb_debug_gemm_prefill_bn(bn) == 0
+    try:
+        g = torch.Generator(device=DEV).manual_seed(bn + 7)
+        T, O, K = 1023, 4096, 1024
+        x = torch.randn(T, K, device=DEV, generator=g).bfloat16()
+        w = (torch.randn(O, K, device=DEV, generator=g) * 0.05).bfloat16()
+        b = torch.randn(O, device=DEV, generator=g).bfloat16()
+        r = torch.randn(T, O, device=DEV, generator=g).bfloat16()
+        y = ops.linear(x, w, bias=b, residual=r, mode=1, num_sms=84, scratch=scratch)
+        I = 1792
+        gate = (torch.randn(I, K, device=DEV, generator=g) * 0.05).bfloat16()
+        up = (torch.randn(I, K, device=DEV, generator=g) * 0.05).bfloat16()
+        wgu = interleave_gate_up(gate, up).contiguous()
+        a = torch.empty(T, I, device=DEV, dtype=torch.bfloat16)
+        lib.rb_gemm_bf16(x.data_ptr(), wgu.data_ptr(), a.data_ptr(), None, None, T, 2 * I, K, K, K, I, 1 | 4, 84,
+                         scratch.ws.data_ptr(), scratch.ws_bytes, scratch.counters.data_ptr(), scratch.counters.numel(),
+                         torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+    finally:
+        lib.rb_debug_gemm_prefill_bn(0)
+    assert rel_l2(y, x.float() @ w.float().T + b.float() + r.float()) < 1e-2
+    ref = torch.nn.functional.silu(x.float() @ gate.float().T) * (x.float() @ up.float().T)
+    assert rel_l2(a, ref) < 1e-2
+
+
+def test_prefill_tile_width_rejects_bad_values():
+    lib = ops.load()
+    assert lib.rb_debug_gemm_prefill_bn(100) != 0
+    assert lib.rb_debug_gemm_prefill_bn(512) != 0
+    assert lib.rb_debug_gemm_prefill_bn(0) == 0
+
+
 @pytest.mark.parametrize("T,mode,sms", [(1, 2, 148), (1, 2, 64), (37, 2, 148), (37, 2, 64), (200, 2, 148),
                                         (300, 1, 148), (1023, 1, 148)])
 @pytest.mark.parametrize("I", [1024, 3584])
