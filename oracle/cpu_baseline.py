@@ -94,6 +94,50 @@ def run_sample(arch, prompt_len: int, out_len: int, batch: int = 8, decode_steps
     }
 
 
+class CpuSampler:
+    """The oracle model and a mid-generation KV state built once; each `step()` is one bounded
+    sample of the workload (one prefill chunk + one batched decode step), so a bench run can
+    take W warm-up and K timed steps of it (bench.py --impl reference)."""
+
+    def __init__(self, arch, prompt_len: int, out_len: int, batch: int = 4, prefill_tokens: int = 16,
+                 threads: int | None = None):
+        self.threads = threads or os.cpu_count() or 1
+        torch.set_num_threads(self.threads)
+        self.arch, self.prompt_len, self.out_len = arch, prompt_len, out_len
+        self.batch, self.prefill_tokens = batch, prefill_tokens
+        t0 = time.perf_counter()
+        self.orc = Oracle(arch, fast_state(arch))
+        self.ctx = prompt_len + out_len // 2
+        self.kvs = [[(torch.randn(self.ctx + 64, arch.kv_heads, arch.head_dim),
+                      torch.randn(self.ctx + 64, arch.kv_heads, arch.head_dim)) for _ in range(arch.layers)]
+                    for _ in range(batch)]
+        self.t_init = time.perf_counter() - t0
+        self.n = 0
+
+    def step(self) -> dict:
+        """One prefill chunk of `prefill_tokens` + one decode step of `batch` rows."""
+        arch = self.arch
+        ids = torch.randint(0, arch.vocab, (self.prefill_tokens,))
+        step_ids = torch.randint(0, arch.vocab, (self.batch,))
+        with torch.no_grad():
+            t0 = time.perf_counter()
+            self.orc.forward(ids, 0, None)
+            t1 = time.perf_counter()
+            decode_batch(self.orc, step_ids, [self.ctx + (self.n % 64)] * self.batch, self.kvs)
+            t2 = time.perf_counter()
+        self.n += 1
+        t_pref = (t1 - t0) / self.prefill_tokens
+        t_dec = (t2 - t1) / self.batch
+        return {"t_prefill_per_token_s": t_pref, "t_decode_per_token_s": t_dec, "wall_s": t2 - t0,
+                "value": 1.0 / (t_dec + (self.prompt_len / self.out_len) * t_pref)}
+
+    def describe(self) -> str:
+        return (f"fp32 CPU oracle ({self.arch.name}, random weights), per step: 1 prefill chunk of "
+                f"{self.prefill_tokens} tokens + 1 batched decode step of B={self.batch} at ctx {self.ctx}; "
+                f"tokens/s = 1/(t_dec + {self.prompt_len}/{self.out_len} * t_prefill) from the median per-token "
+                f"times of the timed steps; model + KV build {self.t_init:.1f} s excluded")
+
+
 if __name__ == "__main__":
     from paper_2601_11822_b200.specs import ARCHS
 
