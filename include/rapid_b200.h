@@ -33,6 +33,10 @@ const char* rb_last_error(void);
 int rb_device_sm_count(int device, int* out);
 /* Debug: when buf != NULL, every GEMM CTA writes 8 globaltimer stamps to buf[8*cta..]. */
 int rb_debug_gemm_trace(unsigned long long* buf);
+/* Debug (profiling probe): push the regular context of green partition i of a
+ * rb_green_split handle onto this thread / pop it again. */
+int rb_debug_green_ctx_push(void* handle, int i);
+int rb_debug_ctx_pop(void);
 /* Debug: GEMM CTA-pair policy, -1 auto (default), 0 force single-CTA, 1 force 2-CTA pairs. */
 int rb_debug_gemm_pair_mode(int mode);
 /* Debug: decode (swap-AB) GEMM schedule, -1 auto (default); else bit0 = two 128-row weight
@@ -82,17 +86,12 @@ int rb_decode_attention(const void* q, long long q_tok_stride, const void* cache
                         int head_dim, int max_pages, float scale, int num_blocks, int num_sms, void* stream);
 
 /* K2 — causal prefill attention of one chunk (positions start..start+T-1)
- * against the paged cache [0, start+T). Replaces the attention share of
- * prefill_time's compute term (costmodel.py:104) for the chunk priced at
- * pkg/src/pdsim/engines/rapid.py:313. */
-int rb_prefill_attention(const void* q, long long q_tok_stride, const void* cache_layer, const int* block_table_row,
-                         int T, int start, int Hq, int Hkv, int head_dim, void* out, long long out_tok_stride,
-                         float scale, void* stream);
-
-/* K2 on tcgen05: same contract as rb_prefill_attention, computed with
- * tcgen05.mma (S = QK^T and O = PV accumulate in TMEM), Q and paged K/V fed by
- * TMA. num_blocks = pages in the cache layer (TMA extent). */
-int rb_prefill_attention_tc(const void* q, long long q_tok_stride, const void* cache_layer,
+ * against the paged cache [0, start+T), on tcgen05 (S = QK^T and O = PV
+ * accumulate in TMEM, Q and paged K/V fed by TMA). Replaces the attention share
+ * of prefill_time's compute term (costmodel.py:104) for the chunk priced at
+ * pkg/src/pdsim/engines/rapid.py:313. num_blocks = pages in the cache layer
+ * (TMA extent). */
+int rb_prefill_attention(const void* q, long long q_tok_stride, const void* cache_layer,
                             const int* block_table_row, int T, int start, int Hq, int Hkv, int head_dim, void* out,
                             long long out_tok_stride, float scale, int num_blocks, void* stream);
 

@@ -46,10 +46,32 @@ def inv_freq(arch) -> torch.Tensor:
     return f
 
 
-def init_state(arch, seed: int = 0, std: float = 0.02, bf16_round: bool = True) -> dict:
-    """Deterministic random weights (CPU generator), optionally rounded to bf16 values."""
+# Frozen cfg-1 init ("confident"): see init_state.
+CONFIDENT_EMBED_STD = 1.0
+CONFIDENT_LM_SCALE = 0.02
+
+
+def init_state(arch, seed: int = 0, std: float = 0.02, bf16_round: bool = True, style: str = "auto") -> dict:
+    """Deterministic weights (CPU generator), optionally rounded to bf16 values.
+
+    style "random": every matrix N(0, std), norms 1 + N(0, 0.1).
+    style "confident" (the frozen cfg-1 tiny decoder, default for arch "tiny"): the same
+    random blocks, but the token embedding has unit std and lm_head is a fixed random row
+    permutation of it times CONFIDENT_LM_SCALE (lm_head[succ(v)] = s * embed[v]). The
+    residual stream then carries the current token's embedding next to the blocks'
+    context-dependent output (comparable norms), so every logit row is one clear top-1
+    (the successor of the current token, ~20 sigma above the rest) plus a context-dependent
+    part that holds most of the row's L2 mass. Greedy ids are therefore stable under bf16
+    rounding (greedy-id exactness is decidable), while the per-step logits rel-L2 check
+    still sees the attention / paged-KV numerics. Random N(0, 0.02) logits have top-1 gaps
+    of ~0.25 sigma, so over a ~1k-token trace some gap always falls inside the bf16 error
+    (SURVEY.md §7.3.6)."""
     g = torch.Generator().manual_seed(seed)
     H, D, I, V = arch.hidden, arch.head_dim, arch.intermediate, arch.vocab
+    if style == "auto":
+        style = "confident" if arch.name == "tiny" else "random"
+    if style not in ("random", "confident"):
+        raise ValueError(f"unknown init style {style!r}")
 
     def w(*shape):
         x = torch.randn(*shape, generator=g) * std
@@ -59,7 +81,11 @@ def init_state(arch, seed: int = 0, std: float = 0.02, bf16_round: bool = True) 
         x = 1.0 + 0.1 * torch.randn(size, generator=g)
         return x.to(torch.bfloat16).float() if bf16_round else x
 
-    st = {"embed": w(V, H)}
+    if style == "confident":
+        e = torch.randn(V, H, generator=g) * CONFIDENT_EMBED_STD
+        st = {"embed": e.to(torch.bfloat16).float() if bf16_round else e}
+    else:
+        st = {"embed": w(V, H)}
     for i in range(arch.layers):
         p = f"layers.{i}."
         st[p + "ln1"] = n(H)
@@ -76,7 +102,14 @@ def init_state(arch, seed: int = 0, std: float = 0.02, bf16_round: bool = True) 
         st[p + "up"] = w(I, H)
         st[p + "down"] = w(H, I)
     st["norm"] = n(H)
-    if not arch.tie_embeddings:
+    if style == "confident":
+        if arch.tie_embeddings:
+            raise ValueError("the confident init needs an untied lm_head")
+        succ = torch.randperm(V, generator=g)
+        lm = torch.empty(V, H)
+        lm[succ] = st["embed"] * CONFIDENT_LM_SCALE
+        st["lm_head"] = lm.to(torch.bfloat16).float() if bf16_round else lm
+    elif not arch.tie_embeddings:
         st["lm_head"] = w(V, H)
     return st
 

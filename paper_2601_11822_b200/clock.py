@@ -9,8 +9,9 @@ event at start + priced duration.
 
 `RealTimeLoop` keeps the same engine-facing API but its clock is the host's
 monotonic microsecond clock since `run()` started. Timed events (arrivals,
-SIM_END) fire when the wall clock reaches them; GPU completions fire when
-their CUDA event reports done (polled), stamped with the observation time.
+SIM_END) fire when the wall clock reaches them, stamped with their due time;
+GPU completions fire when their CUDA event reports done (polled), stamped
+with the observation time.
 """
 
 from __future__ import annotations
@@ -166,35 +167,37 @@ class RealTimeLoop:
         handler(self, ev)
 
     def run(self, handler: Callable[[Any, Event], None]) -> None:
+        """Poll loop. At each poll (host time `now`): first every timed event due by `now`
+        (arrivals, SIM_END) at its due time, then every GPU completion observed done at
+        this poll, stamped `now`, in submission order. Timed events therefore carry their
+        exact trace time (due times are >= every earlier stamp: anything due at or before
+        the previous poll was dispatched there), and the dispatched timeline is the one a
+        virtual-clock replay reproduces with (arrival, seq) / (completion, seq) ordering
+        (tests/test_trace_replay.py)."""
         self._t0 = time.perf_counter_ns()
         while self._timed or self._pending:
             now = self.clock_us()
-            progressed = False
-            # GPU completions first (they free resources for arrivals at the same instant)
+            done = []
             if self._pending:
                 still = []
-                done = []
                 for h, ev in self._pending:
                     (done if h.done() else still).append((h, ev))
                 if done:
                     self._pending = still
-                    now = self.clock_us()
-                    # keep causality monotone
-                    now = max(now, self.now_us)
-                    for h, ev in done:
-                        ev.time_us = now
-                        ev.data["gpu_us"] = h.gpu_us
-                        self.now_us = now
-                        self._dispatch(ev, handler)
-                    progressed = True
-            if self._timed and self._timed[0][0] <= now:
-                while self._timed and self._timed[0][0] <= now:
-                    ev = heapq.heappop(self._timed)[2]
-                    # timed events are stamped with their due time (trace arrivals are exact)
-                    self.now_us = max(self.now_us, ev.time_us)
-                    ev.time_us = self.now_us
-                    self._dispatch(ev, handler)
+            progressed = bool(done)
+            while self._timed and self._timed[0][0] <= now:
+                ev = heapq.heappop(self._timed)[2]
+                self.now_us = max(self.now_us, ev.time_us)
+                ev.time_us = self.now_us
+                self._dispatch(ev, handler)
                 progressed = True
+            if done:
+                now = max(now, self.now_us)
+                for h, ev in done:
+                    ev.time_us = now
+                    ev.data["gpu_us"] = h.gpu_us
+                    self.now_us = now
+                    self._dispatch(ev, handler)
             if not progressed:
                 if not self._pending and self._timed:
                     wait = self._timed[0][0] - self.clock_us()

@@ -9,9 +9,6 @@ int decode_attention_launch(const void* q, long long q_tok_stride, const void* c
                             int bt_stride, const int* row_slot, const int* seq_lens, void* out,
                             long long out_tok_stride, void* workspace, size_t ws_bytes, int B, int Hq, int Hkv,
                             int head_dim, int max_pages, float scale, int num_blocks, int num_sms, cudaStream_t st);
-int prefill_attention_launch(const void* q, long long q_tok_stride, const void* cache_layer, const int* bt, int T,
-                             int start, int Hq, int Hkv, int head_dim, void* out, long long out_tok_stride,
-                             float scale, cudaStream_t st);
 int rmsnorm_launch(const void* x, long long ldx, const void* w, void* y, long long ldy, int T, int H, float eps,
                    cudaStream_t st);
 int rope_cache_launch(const void* qkv, long long ld_qkv, const int* pos, const int* tok_slot, const int* bt,
@@ -82,14 +79,7 @@ int rb_decode_attention(const void* q, long long q_tok_stride, const void* cache
                                      num_blocks, num_sms, ST(stream));
 }
 
-int rb_prefill_attention(const void* q, long long q_tok_stride, const void* cache_layer, const int* block_table_row,
-                         int T, int start, int Hq, int Hkv, int head_dim, void* out, long long out_tok_stride,
-                         float scale, void* stream) {
-  return rb::prefill_attention_launch(q, q_tok_stride, cache_layer, block_table_row, T, start, Hq, Hkv, head_dim, out,
-                                      out_tok_stride, scale, ST(stream));
-}
-
-int rb_prefill_attention_tc(const void* q, long long q_tok_stride, const void* cache_layer,
+int rb_prefill_attention(const void* q, long long q_tok_stride, const void* cache_layer,
                             const int* block_table_row, int T, int start, int Hq, int Hkv, int head_dim, void* out,
                             long long out_tok_stride, float scale, int num_blocks, void* stream) {
   return rb::prefill_attention_tc_launch(q, q_tok_stride, cache_layer, block_table_row, T, start, Hq, Hkv, head_dim,
@@ -203,4 +193,32 @@ int rb_green_destroy(void* handle) {
   return 0;
 }
 
+}  // extern "C"
+
+// Profiling probe: make the (regular) context of green partition i current on this thread,
+// so launches can be issued with the green context current instead of through a green
+// stream from the primary context.
+typedef CUresult (*PFN_cuCtxFromGreenCtx)(CUcontext*, CUgreenCtx);
+typedef CUresult (*PFN_cuCtxPushCurrent)(CUcontext);
+typedef CUresult (*PFN_cuCtxPopCurrent)(CUcontext*);
+extern "C" {
+int rb_debug_green_ctx_push(void* handle, int i) {
+  RB_SYM(PFN_cuCtxFromGreenCtx, cuCtxFromGreenCtx);
+  RB_SYM(PFN_cuCtxPushCurrent, cuCtxPushCurrent);
+  GreenSplit* gs = reinterpret_cast<GreenSplit*>(handle);
+  CUcontext c;
+  CUresult r = cuCtxFromGreenCtx(&c, gs->ctx[i]);
+  if (r != CUDA_SUCCESS) return rb::set_cu_error("cuCtxFromGreenCtx", r);
+  r = cuCtxPushCurrent(c);
+  if (r != CUDA_SUCCESS) return rb::set_cu_error("cuCtxPushCurrent", r);
+  return 0;
+}
+
+int rb_debug_ctx_pop(void) {
+  RB_SYM(PFN_cuCtxPopCurrent, cuCtxPopCurrent);
+  CUcontext c;
+  CUresult r = cuCtxPopCurrent(&c);
+  if (r != CUDA_SUCCESS) return rb::set_cu_error("cuCtxPopCurrent", r);
+  return 0;
+}
 }  // extern "C"

@@ -18,9 +18,6 @@ int decode_attention_launch(const void* q, long long q_tok_stride, const void* c
                             int bt_stride, const int* row_slot, const int* seq_lens, void* out,
                             long long out_tok_stride, void* workspace, size_t ws_bytes, int B, int Hq, int Hkv,
                             int head_dim, int max_pages, float scale, int num_blocks, int num_sms, cudaStream_t st);
-int prefill_attention_launch(const void* q, long long q_tok_stride, const void* cache_layer, const int* bt, int T,
-                             int start, int Hq, int Hkv, int head_dim, void* out, long long out_tok_stride,
-                             float scale, cudaStream_t st);
 int prefill_attention_tc_launch(const void* q, long long q_tok_stride, const void* cache_layer, const int* bt, int T,
                                 int start, int Hq, int Hkv, int head_dim, void* out, long long out_tok_stride,
                                 float scale, int num_blocks, cudaStream_t st);

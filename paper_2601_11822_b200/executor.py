@@ -21,6 +21,7 @@ real kernels on green-context streams.
 
 from __future__ import annotations
 
+from collections import deque
 from dataclasses import dataclass
 
 from paper_2601_11822_b200.arm import decode_time, hybrid_time, overlapped_times, prefill_time
@@ -102,3 +103,45 @@ class CostModelExecutor:
 
     def on_finish(self, req) -> None:
         pass
+
+
+class ReplayExecutor(CostModelExecutor):
+    """Device = the durations a GPU run measured, replayed in launch order (trace replay,
+    SURVEY.md §8(c)). Every launch of a phase returns the next recorded (completion -
+    launch) time of that phase, so a virtual-clock run with cpu_us = 0 dispatches the same
+    timeline the real-time run observed, and its admission / ordering / preemption / ARM
+    decisions can be compared with the GPU run's (and with the reference RapidEngine's,
+    replayed the same way)."""
+
+    def __init__(self, launch_log, num_blocks: int | None = None, block_size: int = 16):
+        self.q = {"prefill": deque(), "decode": deque()}
+        for phase, start, end in launch_log:
+            self.q[phase].append(int(end) - int(start))
+        self.num_blocks = num_blocks
+        self.block_size = block_size
+
+    def make_pool(self, model, gpu):
+        from paper_2601_11822_b200.blockpool import BlockPool
+
+        if self.num_blocks is None:
+            return BlockPool.for_device(model, gpu, name="gpu0")
+        return BlockPool(self.num_blocks, self.block_size, name="gpu0")
+
+    def _next(self, phase: str) -> int:
+        if not self.q[phase]:
+            raise RuntimeError(f"replay diverged: more {phase} launches than the GPU run recorded")
+        return self.q[phase].popleft()
+
+    def launch_prefill(self, req, written, chunk, target, decision, co_decode) -> PricedHandle:
+        cu = decision.cu_fraction_prefill if decision.mode is AllocationMode.PARTITION else 1.0
+        return PricedHandle(self._next("prefill"), cu, "prefill")
+
+    def launch_decode(self, members, decision, co_prefill_chunk) -> PricedHandle:
+        cu = decision.cu_fraction_decode if decision.mode is AllocationMode.PARTITION else 1.0
+        return PricedHandle(self._next("decode"), cu, "decode", tuple(members))
+
+    def launch_hybrid(self, members, head, written, chunk, target) -> PricedHandle:
+        raise NotImplementedError("trace replay covers the RAPID engine")
+
+    def exhausted(self) -> bool:
+        return not self.q["prefill"] and not self.q["decode"]

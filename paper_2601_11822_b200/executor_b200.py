@@ -78,7 +78,8 @@ class B200Executor:
                  static_decode_sms: int | None = None, max_batch: int = 256, chunk_tokens: int = 2048,
                  num_blocks: int | None = None, kv_memory_fraction: float = 0.90, max_context: int | None = None,
                  num_slots: int = 1024, device: str = "cuda", token_source=None, use_graphs: bool = True,
-                 batch_grid: tuple[int, ...] = DEFAULT_BATCH_GRID, serialize_phases: bool = False):
+                 batch_grid: tuple[int, ...] = DEFAULT_BATCH_GRID, serialize_phases: bool = False,
+                 record_logits: bool = False):
         self.arch = arch
         dev = torch.device(device)
         self.device = dev if dev.index is not None else torch.device("cuda", torch.cuda.current_device())
@@ -126,6 +127,9 @@ class B200Executor:
         self._pre_ids_host = torch.zeros(max(chunk_tokens, 16), dtype=torch.int32, pin_memory=True)
         self._pre_ids_dev = torch.zeros(max(chunk_tokens, 16), dtype=torch.int32, device=self.device)
         self.generated: dict[int, list[int]] = {}
+        # parity tests: fp32 host copy of the logits row behind every generated token
+        self.record_logits = record_logits
+        self.logits: dict[int, list[torch.Tensor]] = {}
         self._tokens_cache: dict[int, torch.Tensor] = {}
         # partitions
         self._partitions: dict[int | None, _Partition] = {}
@@ -141,6 +145,7 @@ class B200Executor:
         self.decode_steps = 0
         self.prefill_chunks = 0
         self.gpu_launches = 0
+        self.lazy_captures = 0
         self.step_log: list[tuple[int, int, int]] = []  # (B, gpu_us, host launch ns)
         self.prefill_log: list[tuple[int, int]] = []  # (gpu_us, host launch ns)
 
@@ -195,6 +200,13 @@ class B200Executor:
     def on_release(self, req_id: int) -> None:
         s = self._slot_of.pop(req_id, None)
         if s is not None:
+            # page grants still queued for this slot belong to the released request (e.g. a
+            # decode extension of a member preempted in the same reservation pass): drop
+            # them, or they would land after the slot's next owner writes its rows on the
+            # other stream
+            for q in self._upd.values():
+                if any(u[0] == s for u in q):
+                    q[:] = [u for u in q if u[0] != s]
             self._free_slots.append(s)
 
     def _flush_updates(self, phase: str, stream) -> None:
@@ -326,15 +338,31 @@ class B200Executor:
             return g
         r = self.runner
         st = part.ds
-        # warm up outside capture (tensor-map cache, function attributes)
-        r.decode_body(bucket, num_sms=part.d_sms, stream=st.cuda_stream)
+        # A decode step is not idempotent (argmax overwrites last_tok[slot], the QKV epilogue
+        # writes KV at pos), so the eager warm-up must not run on live inputs: a lazy capture
+        # during serving parks the step's inputs, warms up on padding rows only, and restores
+        # them before the replay (stream-ordered on the decode stream).
+        with torch.cuda.stream(st):
+            live = self._dec_in_dev.clone()
+            self._inert_decode_inputs()
+            # warm up outside capture (tensor-map cache, function attributes)
+            r.decode_body(bucket, num_sms=part.d_sms, stream=st.cuda_stream)
         st.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=st):
             r.decode_body(bucket, num_sms=part.d_sms, stream=st.cuda_stream)
+        with torch.cuda.stream(st):
+            self._dec_in_dev.copy_(live)
         st.synchronize()
         part.graphs[bucket] = g
+        self.lazy_captures += 1
         return g
+
+    def _inert_decode_inputs(self) -> None:
+        """Padding rows only: dummy slot, no KV write (pos -1), empty context."""
+        self._dec_in_dev[0].fill_(self.runner.dummy_slot)
+        self._dec_in_dev[1].fill_(-1)
+        self._dec_in_dev[2].fill_(0)
 
     def warmup(self, decode_sms_list=None) -> None:
         """Pre-capture decode graphs for every bucket on the partitions in use."""
@@ -342,15 +370,12 @@ class B200Executor:
             return
         keys = decode_sms_list if decode_sms_list is not None else (
             [self.static_decode_sms] if self.static_decode_sms is not None else [None])
-        # padding rows only: make the workspace inputs inert for the warm-up replays
-        self._dec_in_dev[0].fill_(self.runner.dummy_slot)
-        self._dec_in_dev[1].fill_(-1)
-        self._dec_in_dev[2].fill_(0)
         for k in keys:
             part = self._partition(k) if k is not None else self._partitions[None]
             for b in self.grid:
                 self._capture(part, b)
         torch.cuda.synchronize()
+        self.lazy_captures = 0  # captures counted from here on happened while serving
 
     def launch_decode(self, members, decision, co_prefill_chunk) -> GpuHandle:
         part = self._pick(decision)
@@ -381,9 +406,12 @@ class B200Executor:
         if handle is None:
             return
         out = self._dec_out_host[: len(handle.members)].tolist()
-        for r, is_lame, tok in zip(handle.members, handle.lame, out):
+        rows = self.runner.dec.logits[: len(handle.members)].float().cpu() if self.record_logits else None
+        for i, (r, is_lame, tok) in enumerate(zip(handle.members, handle.lame, out)):
             if not is_lame:
                 self.generated.setdefault(r.id, []).append(tok)
+                if rows is not None:
+                    self.logits.setdefault(r.id, []).append(rows[i])
         self.step_log.append((len(handle.members), handle.gpu_us, handle.launch_ns))
 
     # ------------------------------------------------------------------ hybrid (K9 fused iteration)
@@ -490,9 +518,15 @@ class HybridB200Executor(B200Executor):
         if handle is None:
             return
         B = len(handle.members)
-        out = self._hyb_out_host[: B + (1 if handle.req is not None else 0)].tolist()
-        for r, tok in zip(handle.members, out):
+        n = B + (1 if handle.req is not None else 0)
+        out = self._hyb_out_host[:n].tolist()
+        rows = self.runner.pre.logits[:n].float().cpu() if self.record_logits else None
+        for i, (r, tok) in enumerate(zip(handle.members, out)):
             self.generated.setdefault(r.id, []).append(tok)
+            if rows is not None:
+                self.logits.setdefault(r.id, []).append(rows[i])
         if handle.req is not None:
             self.generated.setdefault(handle.req.id, []).append(out[B])
+            if rows is not None:
+                self.logits.setdefault(handle.req.id, []).append(rows[B])
         self.step_log.append((B, handle.gpu_us, handle.launch_ns))

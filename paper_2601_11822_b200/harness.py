@@ -62,3 +62,30 @@ def run_items(label: str, items, model, gpu, params, slo, *, tp: int = 1, engine
     rows = [evaluate_request(r, slo) for r in engine.requests]
     summary = summarize(engine.label, qps, engine.requests, slo, sim.horizon_us, engine.busy_intervals, engine.pools)
     return RunResult(summary, rows, engine, sim.horizon_us)
+
+
+def decision_tuples(decision_log) -> list[tuple]:
+    return [(ph, d.mode.value, d.cu_fraction_prefill, d.cu_fraction_decode, d.slo_risk) for ph, d in decision_log]
+
+
+def replay_rapid(items, launch_log, model, gpu, params, slo, *, chunk_tokens: int, max_batch: int,
+                 num_blocks: int | None, horizon_us: int | None = None):
+    """Trace replay: re-run RAPID on the virtual clock with every launch
+    priced at the duration a GPU run recorded for it (executor.ReplayExecutor) and no host
+    gap (cpu_us = 0: the real-time engine's launches start at the event that kicked them).
+    Returns the engine; its requests / decision_log / pool occupancy are then comparable
+    with the GPU run's."""
+    from paper_2601_11822_b200.engines.rapid import RapidEngine
+    from paper_2601_11822_b200.executor import ReplayExecutor
+
+    ex = ReplayExecutor(launch_log, num_blocks)
+    eng = RapidEngine(model, gpu, params, slo, chunk_tokens=chunk_tokens, max_batch=max_batch, executor=ex,
+                      record_decisions=True, record_launches=True)
+    eng.cpu_us = 0
+    sim = Simulation(until_us=horizon_us)
+    eng.prime(sim, items)
+    sim.run(eng.on_event)
+    check_invariants(eng)
+    if not ex.exhausted():
+        raise RuntimeError("replay diverged: the GPU run recorded launches the replay never made")
+    return eng

@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from pathlib import Path
 
 import torch
@@ -46,10 +47,6 @@ _SIGS = {
         _c_int,
     ),
     "rb_prefill_attention": (
-        [_vp, _c_ll, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _c_ll, _c_float, _vp],
-        _c_int,
-    ),
-    "rb_prefill_attention_tc": (
         [_vp, _c_ll, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _c_ll, _c_float, _c_int, _vp],
         _c_int,
     ),
@@ -74,6 +71,8 @@ _SIGS = {
         _c_int,
     ),
     "rb_green_destroy": ([_vp], _c_int),
+    "rb_debug_green_ctx_push": ([_vp, _c_int], _c_int),
+    "rb_debug_ctx_pop": ([], _c_int),
     "rb_tp_nccl_available": ([], _c_int),
     "rb_tp_nccl_unique_id": ([_vp], _c_int),
     "rb_tp_nccl_comm_init": ([_vp, _c_int, _c_int, ctypes.POINTER(_vp)], _c_int),
@@ -139,6 +138,8 @@ def load(path: str | Path | None = None) -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
+    if os.environ.get("RB_PDL", "1") == "0":  # programmatic dependent launch off (profiling A/B)
+        lib.rb_set_pdl(0)
     _LIB = lib
     return lib
 
@@ -245,27 +246,16 @@ def decode_attention(q: torch.Tensor, cache_layer: torch.Tensor, block_table: to
 
 
 def prefill_attention(q: torch.Tensor, cache_layer: torch.Tensor, block_table_row: torch.Tensor, start: int,
-                      out: torch.Tensor, *, num_kv_heads: int, scale: float | None = None, impl: str = "tc",
+                      out: torch.Tensor, *, num_kv_heads: int, scale: float | None = None,
                       stream=None) -> torch.Tensor:
-    """q, out: [T, Hq, D] for chunk positions start..start+T-1 of one request.
-
-    impl "tc": tcgen05/TMEM/TMA kernel (default); "mma": GQA-packed mma.sync kernel."""
+    """q, out: [T, Hq, D] for chunk positions start..start+T-1 of one request (tcgen05/TMEM/TMA kernel)."""
     _need_cuda(q, cache_layer, block_table_row, out)
     T, Hq, D = q.shape
     sc = scale if scale is not None else 1.0 / math.sqrt(D)
-    if impl == "tc":
-        _check(
-            load().rb_prefill_attention_tc(
-                _ptr(q), q.stride(0), _ptr(cache_layer), _ptr(block_table_row), T, start, Hq, num_kv_heads, D,
-                _ptr(out), out.stride(0), sc, cache_layer.shape[0], _stream(stream),
-            ),
-            "rb_prefill_attention_tc",
-        )
-        return out
     _check(
         load().rb_prefill_attention(
-            _ptr(q), q.stride(0), _ptr(cache_layer), _ptr(block_table_row), T, start, Hq, num_kv_heads, D, _ptr(out),
-            out.stride(0), sc, _stream(stream),
+            _ptr(q), q.stride(0), _ptr(cache_layer), _ptr(block_table_row), T, start, Hq, num_kv_heads, D,
+            _ptr(out), out.stride(0), sc, cache_layer.shape[0], _stream(stream),
         ),
         "rb_prefill_attention",
     )

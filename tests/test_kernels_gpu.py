@@ -223,10 +223,9 @@ def test_decode_attention_padded_rows():
     assert rel_l2(out[3:4], _ref_attn(q[3:4], k, v)) < 1e-2
 
 
-@pytest.mark.parametrize("impl", ["tc", "mma"])
 @pytest.mark.parametrize("T,start,Hq,Hkv", [(100, 0, 8, 2), (64, 37, 8, 2), (200, 130, 32, 8), (1, 50, 40, 8),
                                             (257, 0, 8, 1), (300, 500, 32, 8), (1100, 0, 8, 2), (1300, 700, 8, 2)])
-def test_prefill_attention(T, start, Hq, Hkv, impl):
+def test_prefill_attention(T, start, Hq, Hkv):
     # (1100, 0): 9 query tiles from position 0 -> one tile per CTA in the tcgen05 kernel; the
     # others run two tiles per CTA (paired warpgroups sharing K/V)
     gen = torch.Generator(device=DEV).manual_seed(T + start)
@@ -236,7 +235,7 @@ def test_prefill_attention(T, start, Hq, Hkv, impl):
     assert (start + T + 15) // 16 <= 160
     q = torch.randn(T, Hq, D, device=DEV, generator=gen).bfloat16()
     out = torch.empty(T, Hq, D, device=DEV, dtype=torch.bfloat16)
-    ops.prefill_attention(q, cache, bt_row, start, out, num_kv_heads=Hkv, impl=impl)
+    ops.prefill_attention(q, cache, bt_row, start, out, num_kv_heads=Hkv)
     torch.cuda.synchronize()
     k, v = _gather_kv(cache, bt_row, start + T)
     ref = _ref_attn(q, k, v, causal_offset=start)
@@ -260,15 +259,14 @@ def test_prefill_attention_growing_max(T, start):
     k = cache[pages, 0].float() * ramp  # [pages, Hkv, 16, D]: later keys score much higher
     cache[pages, 0] = k.bfloat16()
     out = torch.empty(T, Hq, D, device=DEV, dtype=torch.bfloat16)
-    ops.prefill_attention(q, cache, bt_row, start, out, num_kv_heads=Hkv, impl="tc")
+    ops.prefill_attention(q, cache, bt_row, start, out, num_kv_heads=Hkv)
     torch.cuda.synchronize()
     kk, vv = _gather_kv(cache, bt_row, n)
     assert torch.isfinite(out).all()
     assert rel_l2(out, _ref_attn(q, kk, vv, causal_offset=start)) < 1e-2
 
 
-@pytest.mark.parametrize("impl", ["tc", "mma"])
-def test_prefill_attention_stale_nan_tail(impl):
+def test_prefill_attention_stale_nan_tail():
     """Slots after the chunk end in its last page may never have been written."""
     gen = torch.Generator(device=DEV).manual_seed(99)
     D, nb, Hq, Hkv, T, start = 128, 64, 32, 8, 70, 25
@@ -278,7 +276,7 @@ def test_prefill_attention_stale_nan_tail(impl):
     cache[int(bt_row[n // 16]), :, :, n % 16:] = float("nan")
     q = torch.randn(T, Hq, D, device=DEV, generator=gen).bfloat16()
     out = torch.empty(T, Hq, D, device=DEV, dtype=torch.bfloat16)
-    ops.prefill_attention(q, cache, bt_row, start, out, num_kv_heads=Hkv, impl=impl)
+    ops.prefill_attention(q, cache, bt_row, start, out, num_kv_heads=Hkv)
     torch.cuda.synchronize()
     k, v = _gather_kv(cache, bt_row, n)
     assert torch.isfinite(out).all()
