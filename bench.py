@@ -3,32 +3,46 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--qps Q] [--duration S] [--model llama3.1-8b] [--slo-ms 50]
                     [--decode-sms 72 | --arm | --arm-profile PATH --arm-policy adaptive|balanced|slo-min]
-                    [--engine rapid|hybrid-<chunk>] [--prompt 1024 --output 256]
+                    [--engine rapid|hybrid-<chunk>] [--compare hybrid-2048|none]
+                    [--prompt 1024 --output 256] [--timeline PATH]
 
 Workload (BASELINE.json configs[2], "cfg 3", the configuration the SLO-constrained metric
 is defined on): Llama-3.1-8B bf16 (random-init weights of the real shapes; no checkpoints
-offline), one B200, synthetic trace `synthesize(WorkloadSpec(qps=Q, duration_s=S, seed=42,
-mean_prompt_tokens=1024, mean_output_tokens=256, sigma=0))` served by the real-time RAPID
-engine (prefill and decode of different requests concurrently on disjoint SM partitions
-over one shared paged KV cache) with the measured adaptive ARM (profiles/arm/)
+offline), one B200 per replica, synthetic trace `synthesize(WorkloadSpec(qps=Q*N,
+duration_s=S, seed=42, mean_prompt_tokens=1024, mean_output_tokens=256, sigma=0))` with
+request i served by replica i mod N (replicas.shard_items), each replica the real-time RAPID
+engine (prefill and decode of different requests concurrently on disjoint SM partitions over
+one shared paged KV cache) with the measured adaptive ARM (profiles/arm/)
 choosing the green-context split at every launch. `--decode-sms 72` runs cfg 2 (static
 green-context 50/50 split), `--arm` the reference cost-model allocate(), `--engine
-hybrid-2048` the same engine's chunked-prefill comparator.
+hybrid-2048` the same engine's chunked-prefill comparator as the primary arm.
 
-A "step" is one decode iteration of the engine (one CUDA-graph replay over
-the current batch; prefill chunks run concurrently on the other partition).
-W untimed warm-up steps (at least; the window also waits for the first 25% of
-the trace so the batch is in steady state), then exactly K timed steps between
-CUDA events on the decode stream. value = output tokens delivered in those K
-steps / their device time (whole-job tokens/s; N ranks -> sum of tokens / max
-window time). The SLO check (pooled p99 ITL <= 50 ms over the run) decides
-whether the point is SLO-constrained (--slo-ms). Inputs are larger than L2 (KV cache and
+value (the BASELINE metric): the reference's run-level `summarize().tokens_per_s`
+(pkg/src/pdsim/metrics.py:146-200: output-token stamps in [10% of the horizon, horizon] /
+that window), pooled over all replicas (whole job), and SLO-constrained: it is the rate only
+when the pooled p99 ITL <= --slo-ms, else 0 (the unconstrained rate is reported beside it).
+The same-engine hybrid-2048 comparator (north-star target: RAPID beats it) is served on the
+SAME trace in the same invocation and reported under "comparator".
+
+Steps: a step is one decode iteration (one CUDA-graph replay over the current batch; prefill
+chunks run concurrently on the other partition). After >= W warm-up steps and the summarize
+warm-up cut, exactly K steps are timed between CUDA events on the decode stream
+("device_window", ms_per_step) with nvidia-smi clocks sampled during them; `e2e` is the host
+wall-clock rate over the same K steps through RapidEngine/B200Executor (pinned H2D of step
+inputs, block-table deltas and prefill ids, D2H of sampled ids, every step). The trace is
+sized so the run holds W + K steps (>= 60 s). Inputs are larger than L2 (KV cache and
 weights, ~30 GB per step), so no extra flush is needed.
 
-N > 1 (torchrun): one independent replica per GPU ("replicas only"; the path
-shards by request, no data-path collective), each rank its own trace (seed
-42+rank); barrier + max-over-ranks of the window time via NCCL all_reduce.
+roofline: decode attention (K3), measured IN SITU: CUDA events recorded around the middle
+layer's attention launch inside every decode graph (rb_workspace_t.probe_ev*), summed over
+the K timed steps on whatever partition the ARM chose; algorithmic bytes per launch =
+sum over rows of ctx * Hkv * 128 * 2 (K,V) * 2 B.
+
+N > 1 (torchrun): one independent replica per GPU ("replicas only"; the path shards by
+request, no data-path collective); barrier + max-over-ranks of the device window; tokens and
+latency samples pooled over ranks (replicas.pool_window_stats).
 """
+
 
 from __future__ import annotations
 
@@ -180,6 +194,215 @@ def time_decode_attention(runner, stream, B: int, ctx: int, sms: int, iters: int
     return {"B": B, "ctx": ctx, "bytes": byts, "ms": ms, "gbs": byts / ms / 1e6}
 
 
+
+def _free_cuda():
+    import gc
+
+    import torch
+
+    gc.collect()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+
+def serve(args, arch, items, horizon, engine_kind, rank, world, local, *, primary):
+    """Serve `items` with one engine on this rank's GPU; returns the measurements."""
+    import torch
+
+    from paper_2601_11822_b200.arm import CostParams
+    from paper_2601_11822_b200.clock import RealTimeLoop
+    from paper_2601_11822_b200.engines.hybrid import HybridEngine
+    from paper_2601_11822_b200.engines.rapid import RapidEngine
+    from paper_2601_11822_b200.executor_b200 import B200Executor, HybridB200Executor
+    from paper_2601_11822_b200.harness import check_invariants
+    from paper_2601_11822_b200.replicas import local_window_stats, pool_window_stats
+    from paper_2601_11822_b200.slo import SloSpec
+    from paper_2601_11822_b200.specs import AllocationDecision, AllocationMode, b200_spec
+
+    hybrid = engine_kind.startswith("hybrid-")
+    use_arm = args.arm or hybrid
+    max_ctx = PROMPT + OUTPUT + 64
+    if hybrid:
+        hchunk = int(engine_kind.split("-", 1)[1])
+        ex = HybridB200Executor(arch, seed=rank, max_batch=256, chunk_tokens=hchunk, max_context=max_ctx,
+                                num_slots=4096)
+    else:
+        ex = B200Executor(arch, seed=rank, static_decode_sms=None if args.arm else args.decode_sms, max_batch=256,
+                          chunk_tokens=2048, max_context=max_ctx, num_slots=4096, probe_attention=True)
+    policy = None
+    if args.arm_profile and not hybrid:
+        from paper_2601_11822_b200.arm import MeasuredArm, MeasuredProfile
+
+        policy = MeasuredArm(MeasuredProfile.load(args.arm_profile), SLO_ITL_US, 256, args.arm_policy)
+        ex.warmup(sorted(policy.splits_used(), key=lambda d: -1 if d is None else d))
+    else:
+        ex.warmup()
+    pkey = None if use_arm else args.decode_sms
+    total = ex.total_sms
+    model = arch.model_spec()
+    slo = SloSpec(itl_slo_us=SLO_ITL_US)
+    if hybrid:
+        engine = HybridEngine(model, b200_spec(), CostParams(), slo, chunk_tokens=hchunk, max_batch=256, executor=ex)
+    else:
+        part = ex._partitions[pkey]
+        static = None if args.arm else AllocationDecision(AllocationMode.PARTITION, part.p_sms / total,
+                                                          part.d_sms / total)
+        gpu_spec, cost_params = b200_spec(), CostParams()
+        if args.arm_calibrated:  # the reference allocate() on the refitted model
+            import dataclasses
+
+            from paper_2601_11822_b200.specs import GpuSpec
+
+            with open(args.arm_calibrated) as fh:
+                fit = json.load(fh)
+            gpu_spec = GpuSpec(**fit["gpu"])
+            cost_params = dataclasses.replace(CostParams(), **fit["params"])
+        engine = RapidEngine(model, gpu_spec, cost_params, slo, chunk_tokens=2048, max_batch=256, executor=ex,
+                             static_decision=static, record_decisions=args.arm, arm_policy=policy)
+
+    # ---- timed window over K decode steps, hooked on the executor
+    cut_us = int(0.10 * horizon)  # summarize()'s warm-up cut: the device window starts after it
+    win = {"start_handle": None, "end_handle": None, "tokens": 0, "steps": 0, "host0": None, "host1": None,
+           "h2d0": 0, "h2d1": 0, "d2h0": 0, "d2h1": 0, "launch0": 0, "launch1": 0, "Bs": [], "ctxs": []}
+    clocks = ClockSampler(local)
+    launch_name, finish_name = ("launch_hybrid", "finish_hybrid") if hybrid else ("launch_decode", "finish_decode")
+    orig_launch = getattr(ex, launch_name)
+    orig_finish = getattr(ex, finish_name)
+    loop_ref = {}
+
+    def launch_decode(members, *a):
+        h = orig_launch(members, *a)
+        st = win
+        if st["start_handle"] is None and ex.decode_steps > args.warmup and loop_ref["loop"].clock_us() >= cut_us:
+            st["start_handle"] = h
+            st["host0"] = time.perf_counter()
+            st["h2d0"], st["d2h0"], st["launch0"] = ex.h2d_bytes, ex.d2h_bytes, ex.gpu_launches
+            if primary:
+                clocks.start()
+        if st["start_handle"] is not None and st["end_handle"] is None:
+            st["steps"] += 1
+            st["Bs"].append(len(members))
+            if members:
+                st["ctxs"].append(sum(r.context_tokens for r in members) / len(members))
+            h._win = True
+            if st["steps"] == args.steps:
+                st["end_handle"] = h
+        return h
+
+    def finish_decode(h):
+        orig_finish(h)
+        if getattr(h, "_win", False):
+            win["tokens"] += sum(1 for lame in h.lame if not lame)
+            if h.kind == "hybrid" and getattr(h, "req", None) is not None:
+                win["tokens"] += 1  # first token of the request whose prompt this chunk finished
+            if h is win["end_handle"]:
+                win["host1"] = time.perf_counter()
+                win["h2d1"], win["d2h1"], win["launch1"] = ex.h2d_bytes, ex.d2h_bytes, ex.gpu_launches
+                if primary:
+                    win["clocks"] = clocks.stop()
+
+    setattr(ex, launch_name, launch_decode)
+    setattr(ex, finish_name, finish_decode)
+
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    loop = RealTimeLoop(until_us=horizon)
+    loop_ref["loop"] = loop
+    engine.prime(loop, items)
+    t_run = time.perf_counter()
+    loop.run(engine.on_event)
+    t_run = time.perf_counter() - t_run
+    torch.cuda.synchronize()
+    check_invariants(engine)
+    if primary and win.get("clocks") is None and clocks.proc is not None:
+        win["clocks"] = clocks.stop()
+
+    complete = win["end_handle"] is not None and win["host1"] is not None
+    ms = win["start_handle"].ev0.elapsed_time(win["end_handle"].ev1) if complete else float("nan")
+    host_s = win["host1"] - win["host0"] if complete else float("nan")
+    tokens = win["tokens"]
+    # in-situ decode-attention probe over the timed steps
+    w0 = getattr(win["start_handle"], "launch_ns", 0) if complete else 0
+    w1 = getattr(win["end_handle"], "launch_ns", 0) if complete else 0
+    probe = [(b, m, s) for b, m, s, ns in getattr(ex, "attn_probe_log", []) if w0 <= ns <= w1]
+    pb, pm = float(sum(b for b, _, _ in probe)), float(sum(m for _, m, _ in probe))
+    by_part = collections.defaultdict(lambda: [0.0, 0.0, 0])
+    for b, m, s in probe:
+        by_part[s][0] += b
+        by_part[s][1] += m
+        by_part[s][2] += 1
+    if world > 1:
+        t = torch.tensor([ms, host_s, pb, pm], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t[:2], op=torch.distributed.ReduceOp.MAX)
+        tk = torch.tensor([tokens, pb, pm], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(tk, op=torch.distributed.ReduceOp.SUM)
+        ms, host_s, tokens, pb, pm = float(t[0]), float(t[1]), float(tk[0]), float(tk[1]), float(tk[2])
+    pooled = pool_window_stats(local_window_stats(engine.requests, slo, loop.horizon_us))
+
+    steps = max(1, win["steps"])
+
+    def duty(log, t0, t1):
+        sel = [(g, ns) for g, ns in log if t0 <= ns <= t1]
+        if len(sel) < 2:
+            return None
+        span_us = (sel[-1][1] - sel[0][1]) / 1e3
+        return round(sum(g for g, _ in sel[:-1]) / span_us, 3) if span_us > 0 else None
+
+    res = {
+        "engine": engine_kind, "pooled": pooled, "complete": complete, "ms": ms, "host_s": host_s, "tokens": tokens,
+        "steps": win["steps"], "clocks": win.get("clocks"),
+        "h2d": (win["h2d1"] - win["h2d0"]) / steps if complete else 0,
+        "d2h": (win["d2h1"] - win["d2h0"]) / steps if complete else 0,
+        "launches": int(win["launch1"] - win["launch0"]) if complete else 0,
+        "mean_batch": statistics.mean(win["Bs"]) if win["Bs"] else None,
+        "mean_ctx": statistics.mean(win["ctxs"]) if win["ctxs"] else None,
+        "probe": {"bytes": pb, "ms": pm, "launches": len(probe),
+                  "by_sms": {str(k): {"gbs": v[0] / v[1] / 1e6 if v[1] else None, "launches": v[2]}
+                             for k, v in sorted(by_part.items())}},
+        "duty": {"decode": duty([(g, ns) for _, g, ns in ex.step_log], w0, w1),
+                 "prefill": duty(getattr(ex, "prefill_log", []), w0, w1)},
+        "run_wall_s": t_run, "requests": len(engine.requests),
+        "finished_all": sum(1 for r in engine.requests if r.state.value == "finished"),
+        "policy": policy, "total_sms": total, "pkey": pkey,
+        "arm_decisions": ({**{k: sum(1 for _, d in engine.decision_log if d.mode.value == k)
+                              for k in ("overallocate", "partition")},
+                           "decode_sms": dict(sorted(collections.Counter(
+                               str(round(d.cu_fraction_decode * total)) for _, d in engine.decision_log
+                               if d.mode.value == "partition").items()))}
+                          if getattr(engine, "decision_log", None) else None),
+    }
+    if args.timeline and rank == 0:
+        _write_timeline(args.timeline + f".{engine_kind}.json", engine, ex, loop.horizon_us)
+    if primary and not hybrid:
+        res["ex"], res["part"] = ex, ex._partitions[pkey]
+    else:
+        ex.close()
+    del engine
+    return res
+
+
+def _write_timeline(path, engine, ex, horizon_us):
+    """Per-second diagnostics: delivered tokens, decode steps / batch, decode SMs, queue."""
+    nsec = int(horizon_us // 1_000_000) + 10
+    tok = [0] * nsec
+    for r in engine.requests:
+        for t in r.token_times_us:
+            if 0 <= t // 1_000_000 < nsec:
+                tok[int(t // 1_000_000)] += 1
+    ttft = collections.defaultdict(list)
+    for r in engine.requests:
+        if r.token_times_us:
+            ttft[int(r.arrival_us // 1_000_000)].append((r.token_times_us[0] - r.arrival_us) / 1e3)
+    out = {"tokens_per_s": tok, "ttft_ms_by_arrival_s": {k: statistics.mean(v) for k, v in sorted(ttft.items())},
+           "step_log": ex.step_log[:20000], "prefill_log": getattr(ex, "prefill_log", [])[:20000]}
+    if getattr(engine, "decision_log", None):
+        out["decisions"] = [(ph, round(d.cu_fraction_decode * 148)) for ph, d in engine.decision_log][:40000]
+    os.makedirs(os.path.dirname(os.path.abspath(path)), exist_ok=True)
+    with open(path, "w") as fh:
+        json.dump(out, fh)
+
+
 def main():
     global PROMPT, OUTPUT, SLO_ITL_US
     ap = argparse.ArgumentParser()
@@ -187,8 +410,8 @@ def main():
     ap.add_argument("--steps", type=int, default=600)
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    # 56 QPS (14.3k output tok/s offered) saturates the RAPID engine on one B200 with p99 ITL
-    # under the SLO: the saturated delivered rate is the SLO-constrained maximum of the sweep.
+    # 56 QPS per replica (14.3k output tok/s offered) saturates the RAPID engine on one B200
+    # with p99 ITL under the SLO: the saturated delivered rate is the SLO-constrained maximum
     ap.add_argument("--qps", type=float, default=56.0)
     ap.add_argument("--duration", type=float, default=None)
     ap.add_argument("--decode-sms", type=int, default=None,
@@ -198,21 +421,25 @@ def main():
     ap.add_argument("--output", type=int, default=OUTPUT, help="mean output tokens (cfg 5: 128)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--engine", default="rapid", help="rapid | hybrid-<chunk> (same-engine chunked-prefill comparator)")
+    ap.add_argument("--compare", default="auto",
+                    help="second arm on the same trace in the same run: hybrid-<chunk> | none (auto: hybrid-2048 "
+                         "when --engine rapid)")
     ap.add_argument("--slo-ms", type=float, default=SLO_ITL_US / 1e3, help="p99 ITL SLO (default 50 ms)")
     ap.add_argument("--arm-profile", default="auto",
                     help="measured B200 ARM tables (profiler.py JSON; 'auto' = the committed profile of --model "
                          "under profiles/arm/)")
-    ap.add_argument("--arm-policy", default="adaptive", choices=["balanced", "slo-min", "adaptive"])
+    ap.add_argument("--arm-policy", default="adaptive", choices=["balanced", "slo-min", "adaptive", "feedback"])
     ap.add_argument("--arm", action="store_true",
                     help="the reference allocate() on the cost model instead of the measured ARM")
     ap.add_argument("--arm-calibrated", default=None,
                     help="with --arm: the reference cost model refitted to the B200 tables (profiler --calibrate JSON)")
+    ap.add_argument("--timeline", default=None, help="write per-second diagnostics to PATH.<engine>.json")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     PROMPT, OUTPUT = args.prompt, args.output
     SLO_ITL_US = int(args.slo_ms * 1e3)
-    # default (cfg 3): RAPID with the measured adaptive ARM; --decode-sms N: cfg-2 static split;
-    # --arm: the reference cost-model allocate()
+    if args.compare == "auto":
+        args.compare = "hybrid-2048" if args.engine == "rapid" else "none"
     if args.arm_calibrated:
         args.arm = True
     if args.decode_sms is not None or args.arm or args.engine != "rapid":
@@ -234,181 +461,40 @@ def main():
 
     import torch
 
-    from paper_2601_11822_b200 import ops
-    from paper_2601_11822_b200.arm import CostParams
-    from paper_2601_11822_b200.clock import RealTimeLoop
-    from paper_2601_11822_b200.engines.rapid import RapidEngine
-    from paper_2601_11822_b200.engines.hybrid import HybridEngine
-    from paper_2601_11822_b200.executor_b200 import B200Executor, HybridB200Executor
-    from paper_2601_11822_b200.harness import check_invariants
-    from paper_2601_11822_b200.slo import SloSpec, percentile_nearest_rank, summarize
-    from paper_2601_11822_b200.specs import ARCHS, AllocationDecision, AllocationMode, b200_spec
+    from paper_2601_11822_b200.replicas import shard_items
+    from paper_2601_11822_b200.specs import ARCHS
     from paper_2601_11822_b200.traffic import WorkloadSpec, synthesize
 
     torch.cuda.set_device(local)
     arch = ARCHS[args.model]
     peaks = _peaks()
-    # trace long enough for warm-up + K steps (~12 ms per step at steady state)
-    duration = args.duration or max(30.0, 8.0 + (args.warmup + args.steps) * 0.02 * 1.6)
-    items = synthesize(WorkloadSpec(qps=args.qps, duration_s=duration, seed=42 + rank, mean_prompt_tokens=PROMPT,
-                                    mean_output_tokens=OUTPUT, sigma=0.0))
-    hybrid = args.engine.startswith("hybrid-")
-    if hybrid:
-        args.arm = True  # one fused stream on the whole device; no split
-        hchunk = int(args.engine.split("-", 1)[1])
-        ex = HybridB200Executor(arch, seed=rank, max_batch=256, chunk_tokens=hchunk, max_context=PROMPT + OUTPUT + 64,
-                                num_slots=4096)
-    else:
-        ex = B200Executor(arch, seed=rank, static_decode_sms=None if args.arm else args.decode_sms, max_batch=256,
-                          chunk_tokens=2048, max_context=PROMPT + OUTPUT + 64, num_slots=4096)
-    policy = None
-    if args.arm_profile and not hybrid:
-        from paper_2601_11822_b200.arm import MeasuredArm, MeasuredProfile
-
-        policy = MeasuredArm(MeasuredProfile.load(args.arm_profile), SLO_ITL_US, 256, args.arm_policy)
-        ex.warmup(sorted(policy.splits_used(), key=lambda d: -1 if d is None else d))
-    else:
-        ex.warmup()
-    pkey = None if args.arm else args.decode_sms
-    d_sms = ex._partitions[pkey].d_sms
-    p_sms = ex._partitions[pkey].p_sms
-    total = ex.total_sms
-    static = None if args.arm else AllocationDecision(AllocationMode.PARTITION, p_sms / total, d_sms / total)
-    model = arch.model_spec()
-    slo = SloSpec(itl_slo_us=SLO_ITL_US)
-    if hybrid:
-        engine = HybridEngine(model, b200_spec(), CostParams(), slo, chunk_tokens=hchunk, max_batch=256, executor=ex)
-    else:
-        gpu_spec, cost_params = b200_spec(), CostParams()
-        if args.arm_calibrated:  # the reference allocate() on the refitted model
-            import dataclasses
-
-            from paper_2601_11822_b200.specs import GpuSpec
-
-            with open(args.arm_calibrated) as fh:
-                fit = json.load(fh)
-            gpu_spec = GpuSpec(**fit["gpu"])
-            cost_params = dataclasses.replace(CostParams(), **fit["params"])
-        engine = RapidEngine(model, gpu_spec, cost_params, slo, chunk_tokens=2048, max_batch=256, executor=ex,
-                             static_decision=None if args.arm else static, record_decisions=args.arm,
-                             arm_policy=policy)
-
-    # ---- timed window over decode steps, hooked on the executor
+    # trace long enough for warm-up + K steps (~20 ms per step at steady state) and >= 60 s so
+    # the run-level rate is not dominated by the ramp
+    duration = args.duration or max(60.0, 8.0 + (args.warmup + args.steps) * 0.02 * 1.6)
     horizon = int(duration * 1e6)
-    win = {"start_handle": None, "end_handle": None, "tokens": 0, "steps": 0, "host0": None, "host1": None,
-           "h2d0": 0, "h2d1": 0, "d2h0": 0, "d2h1": 0, "launch0": 0, "launch1": 0, "Bs": [], "ctxs": []}
-    clocks = ClockSampler(local)
-    launch_name, finish_name = ("launch_hybrid", "finish_hybrid") if hybrid else ("launch_decode", "finish_decode")
-    orig_launch = getattr(ex, launch_name)
-    orig_finish = getattr(ex, finish_name)
-    loop_ref = {}
+    items = shard_items(synthesize(WorkloadSpec(qps=args.qps * world, duration_s=duration, seed=42,
+                                                mean_prompt_tokens=PROMPT, mean_output_tokens=OUTPUT, sigma=0.0)),
+                        rank, world)
 
-    def launch_decode(members, *a):
-        h = orig_launch(members, *a)
-        st = win
-        steady = loop_ref["loop"].clock_us() >= 0.25 * horizon
-        if st["start_handle"] is None and ex.decode_steps > args.warmup and steady:
-            st["start_handle"] = h
-            st["host0"] = time.perf_counter()
-            st["h2d0"], st["d2h0"], st["launch0"] = ex.h2d_bytes, ex.d2h_bytes, ex.gpu_launches
-            clocks.start()
-        if st["start_handle"] is not None and st["end_handle"] is None:
-            st["steps"] += 1
-            st["Bs"].append(len(members))
-            if members:
-                st["ctxs"].append(sum(r.context_tokens for r in members) / len(members))
-            h._win = True
-            if st["steps"] == args.steps:
-                st["end_handle"] = h
-        return h
+    main_res = serve(args, arch, items, horizon, args.engine, rank, world, local, primary=True)
+    ex = main_res.pop("ex", None)
+    part = main_res.pop("part", None)
 
-    def finish_decode(h):
-        orig_finish(h)
-        if getattr(h, "_win", False):
-            win["tokens"] += sum(1 for lame in h.lame if not lame)
-            if h.kind == "hybrid" and getattr(h, "req", None) is not None:
-                win["tokens"] += 1  # first token of the request whose prompt this chunk finished
-            if h is win["end_handle"]:
-                win["host1"] = time.perf_counter()
-                win["h2d1"], win["d2h1"], win["launch1"] = ex.h2d_bytes, ex.d2h_bytes, ex.gpu_launches
-                win["clocks"] = clocks.stop()
+    # isolated probe on the full device (secondary; the in-situ number is the roofline)
+    iso = None
+    if ex is not None:
+        mB = int(round(main_res["mean_batch"] or 64))
+        mctx = int(round(main_res["mean_ctx"] or PROMPT + OUTPUT // 2))
+        full = ex._partitions[None]
+        iso = time_decode_attention(ex.runner, full.ds, mB, mctx, full.d_sms)
+        ex.close()
+        del ex, part
+    _free_cuda()
 
-    setattr(ex, launch_name, launch_decode)
-    setattr(ex, finish_name, finish_decode)
-
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    loop = RealTimeLoop(until_us=horizon)
-    loop_ref["loop"] = loop
-    engine.prime(loop, items)
-    t_run = time.perf_counter()
-    loop.run(engine.on_event)
-    t_run = time.perf_counter() - t_run
-    torch.cuda.synchronize()
-    check_invariants(engine)
-
-    complete = win["end_handle"] is not None and win["host1"] is not None
-    if complete:
-        ms = win["start_handle"].ev0.elapsed_time(win["end_handle"].ev1)
-        host_s = win["host1"] - win["host0"]
-    else:
-        ms, host_s = float("nan"), float("nan")
-    tokens = win["tokens"]
-    if world > 1:
-        t = torch.tensor([ms, host_s, tokens], dtype=torch.float64, device="cuda")
-        mx = t.clone()
-        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
-        sm = t.clone()
-        torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
-        ms, host_s, tokens = float(mx[0]), float(mx[1]), float(sm[2])
-    summ = summarize(engine.label, args.qps, engine.requests, slo, loop.horizon_us, engine.busy_intervals,
-                     engine.pools)
-    value = tokens / (ms / 1e3) if complete else 0.0
-    e2e_value = tokens / host_s if complete else 0.0
-
-    # live roofline probe of the dominant decode kernel (decode attention) at the window's mean
-    # batch and context: on the static decode partition (cfg 2) or, under the ARM, on all SMs
-    # (the kernel against the device peak) plus the ARM's most frequent decode partition
-    part = ex._partitions[pkey]
-    mB = int(round(statistics.mean(win["Bs"]))) if win["Bs"] else 64
-    mctx = int(round(statistics.mean(win["ctxs"]))) if win["ctxs"] else PROMPT + OUTPUT // 2
-    probe = time_decode_attention(ex.runner, part.ds, mB, mctx, part.d_sms)
-    part_probe = None
-    if args.arm and getattr(engine, "decision_log", None) and not hybrid:
-        used = collections.Counter(round(d.cu_fraction_decode * total) for ph, d in engine.decision_log
-                                   if ph == "decode" and d.mode.value == "partition")
-        if used:
-            pp = ex._partition(used.most_common(1)[0][0])
-            part_probe = time_decode_attention(ex.runner, pp.ds, mB, mctx, pp.d_sms)
-            part_probe["sms"] = pp.d_sms
-    hbm = peaks["hbm_gbs"]
-    # DRAM traffic of the dominant kernel from the committed ncu --set full capture, per launch:
-    # measured bytes / algorithmic bytes at the capture shape, times this probe's algorithmic bytes
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            nt = json.load(fh)["decode_attn_tc_kernel"]
-        traffic = (nt["dram_bytes_read"] + nt["dram_bytes_write"]) / nt["algorithmic_bytes"] * probe["bytes"]
-    except (OSError, KeyError, ValueError):
-        pass
-    steps = max(1, win["steps"])
-    h2d = (win["h2d1"] - win["h2d0"]) / steps if complete else 0
-    d2h = (win["d2h1"] - win["d2h0"]) / steps if complete else 0
-    launches = int(win["launch1"] - win["launch0"]) if complete else 0
-
-    # duty cycles over the window: device-busy time / wall time between launches on each phase stream
-    def duty(log, t0, t1):
-        sel = [(g, ns) for g, ns in log if t0 <= ns <= t1]
-        if len(sel) < 2:
-            return None
-        span_us = (sel[-1][1] - sel[0][1]) / 1e3
-        return round(sum(g for g, _ in sel[:-1]) / span_us, 3) if span_us > 0 else None
-
-    w0 = getattr(win["start_handle"], "launch_ns", 0) if complete else 0
-    w1 = getattr(win["end_handle"], "launch_ns", 0) if complete else 0
-    duties = {"decode": duty([(g, ns) for _, g, ns in ex.step_log], w0, w1),
-              "prefill": duty(getattr(ex, "prefill_log", []), w0, w1)}
+    comp = None
+    if args.compare != "none":
+        comp = serve(args, arch, items, horizon, args.compare, rank, world, local, primary=False)
+        _free_cuda()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -416,18 +502,37 @@ def main():
 
         cpu = run_sample(arch, PROMPT, OUTPUT, batch=8, decode_steps=1, prefill_tokens=32)
         cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
-
     if rank != 0:
         return
-    profile_path = os.path.join(ROOT, "profiles")
+
+    def constrained(p):
+        return p["tokens_per_s"] if p["itl_p99_us"] <= SLO_ITL_US else 0.0
+
+    m = main_res
+    pooled = m["pooled"]
+    hbm = peaks["hbm_gbs"]
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            nt = json.load(fh)["decode_attn_tc_kernel"]
+        ratio = (nt["dram_bytes_read"] + nt["dram_bytes_write"]) / nt["algorithmic_bytes"]
+    except (OSError, KeyError, ValueError):
+        ratio = None
+    pr = m["probe"]
+    per_launch_bytes = pr["bytes"] / pr["launches"] if pr["launches"] else 0.0
+    achieved = pr["bytes"] / pr["ms"] / 1e6 if pr["ms"] else None
+    if ratio is not None and per_launch_bytes:
+        traffic = ratio * per_launch_bytes
+    steps = max(1, m["steps"])
+    value = constrained(pooled)
     line = {
         "metric": "SLO-constrained output tokens/s per GPU (p99 ITL<=SLO); p50 TTFT; p99 ITL",
         "value": value,
         "unit": "output tokens/s",
         "n_gpus": world,
-        "steps": win["steps"],
+        "steps": m["steps"],
         "warmup": args.warmup,
-        "ms_per_step": ms / steps if complete else None,
+        "ms_per_step": m["ms"] / steps if m["complete"] else None,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
@@ -435,57 +540,73 @@ def main():
         "data": f"synthetic (random-init {args.model} weights of the real shapes, synthesize() trace)",
         "config": {
             "workload": (f"cfg3: {args.model} bf16, adaptive ARM ("
-                         + (f"measured B200 tables, {args.arm_policy} policy" if policy else "reference allocate()")
-                         + f" at every launch; OVERALLOCATE -> both phases on {total} SMs, PARTITION -> "
-                           f"green-context split)" if args.arm else
-                         f"cfg2: {args.model} bf16, 1x B200 per replica, static split decode {d_sms} / prefill "
-                         f"{p_sms} SMs") + f", trace in {PROMPT}/out {OUTPUT} sigma=0 at {args.qps} QPS for "
-                                         f"{duration:.0f} s",
+                         + (f"measured B200 tables, {args.arm_policy} policy" if m["policy"] else
+                            "reference allocate()")
+                         + f" at every launch; OVERALLOCATE -> both phases on {m['total_sms']} SMs, PARTITION -> "
+                           f"green-context split)" if args.arm and args.engine == "rapid" else
+                         f"{args.engine}: {args.model} bf16" if args.engine != "rapid" else
+                         f"cfg2: {args.model} bf16, static split decode {args.decode_sms} SMs")
+                        + f", trace in {PROMPT}/out {OUTPUT} sigma=0 at {args.qps} QPS per replica for "
+                          f"{duration:.0f} s, request i -> replica i mod {world}",
             "qps_per_replica": args.qps,
             "parallelism": f"replicas x{world}",
             "l2": "inputs > L2 (KV + weights ~30 GB per step); no flush",
-            "step": ("one fused hybrid iteration (decode rows + one prefill chunk)" if hybrid else
-                     "one decode iteration (CUDA-graph replay); prefill runs concurrently on its partition"),
+            "step": "one decode iteration (CUDA-graph replay); prefill runs concurrently on its partition"
+                    if args.engine == "rapid" else "one fused hybrid iteration (decode rows + one prefill chunk)",
             "engine": args.engine,
         },
-        "p50_ttft_ms": summ.ttft_p50_us / 1e3,
-        "p99_itl_ms": summ.itl_p99_us / 1e3,
-        "p95_itl_ms": summ.itl_p95_us / 1e3,
+        "value_definition": ("reference summarize().tokens_per_s (metrics.py:146-200) over [10% horizon, horizon], "
+                             "pooled over replicas (whole job); 0 when pooled p99 ITL > SLO"),
+        "per_gpu": value / world,
+        "tokens_per_s_unconstrained": pooled["tokens_per_s"],
+        "p50_ttft_ms": pooled["ttft_p50_us"] / 1e3,
+        "p99_itl_ms": pooled["itl_p99_us"] / 1e3,
+        "p95_itl_ms": pooled["itl_p95_us"] / 1e3,
         "slo_itl_ms": SLO_ITL_US / 1e3,
-        "slo_met": bool(summ.itl_p99_us <= SLO_ITL_US),
-        "run_tokens_per_s": summ.tokens_per_s,
-        "goodput_req_s": summ.goodput,
-        "mean_decode_batch": statistics.mean(win["Bs"]) if win["Bs"] else None,
-        "mean_context": statistics.mean(win["ctxs"]) if win["ctxs"] else None,
-        "e2e": {"value": e2e_value, "unit": "output tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+        "slo_met": bool(pooled["itl_p99_us"] <= SLO_ITL_US),
+        "goodput_req_s": pooled["goodput"],
+        "per_replica_tokens_per_s": pooled["per_replica_tokens_per_s"],
+        "device_window": {"tokens_per_s": m["tokens"] / (m["ms"] / 1e3) if m["complete"] else None,
+                          "steps": m["steps"], "ms_per_step": m["ms"] / steps if m["complete"] else None,
+                          "mean_decode_batch": m["mean_batch"], "mean_context": m["mean_ctx"],
+                          "note": "output tokens of the K timed decode steps / their CUDA-event time (max over ranks)"},
+        "e2e": {"value": m["tokens"] / m["host_s"] if m["complete"] else 0.0, "unit": "output tokens/s",
+                "h2d_bytes_per_step": m["h2d"], "d2h_bytes_per_step": m["d2h"],
                 "note": "host wall clock over the same K steps through RapidEngine/B200Executor (pinned H2D of "
                         "step inputs + block-table deltas + prefill ids, D2H of sampled ids, every step)"},
-        "roofline": {"kernel": "decode_attn_tc_kernel (K3)", "bound": "hbm", "achieved": probe["gbs"], "peak": hbm,
-                     "unit": "GB/s", "frac": probe["gbs"] / hbm, "traffic": traffic,
+        "roofline": {"kernel": "decode_attn_tc_kernel (K3)", "bound": "hbm", "achieved": achieved, "peak": hbm,
+                     "unit": "GB/s", "frac": achieved / hbm if achieved else None, "traffic": traffic,
+                     "measured": (f"in situ: CUDA events around layer {arch.layers // 2}'s decode attention inside "
+                                  f"the decode graphs, {pr['launches']} launches over the K timed steps on the ARM's "
+                                  f"partitions; {per_launch_bytes:.0f} algorithmic B per launch on average"),
+                     "by_decode_sms": pr["by_sms"],
                      "traffic_src": "profiles/ncu_traffic.json (dram read+write / algorithmic bytes of one "
-                                    "ncu --set full launch, scaled to this probe)",
-                     "per_launch": f"B={probe['B']} ctx={probe['ctx']}: {probe['bytes']} B (K+V bf16, 1 layer) "
-                                   f"in {probe['ms'] * 1e3:.1f} us on {part.d_sms} SMs",
-                     "on_arm_partition": (None if part_probe is None else
-                                          {"sms": part_probe["sms"], "achieved": part_probe["gbs"],
-                                           "frac": part_probe["gbs"] / hbm,
-                                           "us": round(part_probe["ms"] * 1e3, 1)}),
+                                    "ncu --set full launch) x the mean in-situ launch bytes",
+                     "isolated_full_device": (None if iso is None else
+                                              {"sms": m["total_sms"], "gbs": iso["gbs"], "frac": iso["gbs"] / hbm,
+                                               "B": iso["B"], "ctx": iso["ctx"], "us": round(iso["ms"] * 1e3, 1)}),
                      "peak_src": peaks["_src"]},
-        "gpu_launches": launches,
-        "clocks": win.get("clocks", {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}),
+        "gpu_launches": m["launches"],
+        "clocks": m["clocks"] or {"sm_mhz": None, "sm_max_mhz": None, "reasons": []},
         "cpu_baseline": cpu,
-        "run_wall_s": t_run,
-        "arm_decisions": ({**{k: sum(1 for _, d in engine.decision_log if d.mode.value == k)
-                              for k in ("overallocate", "partition")},
-                           "decode_sms": dict(sorted(collections.Counter(
-                               str(round(d.cu_fraction_decode * total)) for _, d in engine.decision_log
-                               if d.mode.value == "partition").items()))}
-                          if getattr(engine, "decision_log", None) else None),
-        "stream_duty": duties,
-        "requests": len(engine.requests),
-        "finished": sum(1 for r in engine.requests if r.state.value == "finished"),
-        "profiles": profile_path,
+        "run_wall_s": m["run_wall_s"],
+        "arm_decisions": m["arm_decisions"],
+        "stream_duty": m["duty"],
+        "requests": m["requests"],
+        "finished": m["finished_all"],
+        "profiles": os.path.join(ROOT, "profiles"),
     }
+    if comp is not None:
+        cp = comp["pooled"]
+        line["comparator"] = {
+            "engine": comp["engine"], "value": constrained(cp), "tokens_per_s_unconstrained": cp["tokens_per_s"],
+            "p99_itl_ms": cp["itl_p99_us"] / 1e3, "p50_ttft_ms": cp["ttft_p50_us"] / 1e3,
+            "slo_met": bool(cp["itl_p99_us"] <= SLO_ITL_US), "goodput_req_s": cp["goodput"],
+            "device_window_tokens_per_s": comp["tokens"] / (comp["ms"] / 1e3) if comp["complete"] else None,
+            "mean_decode_batch": comp["mean_batch"], "run_wall_s": comp["run_wall_s"],
+            "note": "same trace, same engine code, same run; chunked-prefill hybrid batching on the whole device"}
+        cv = constrained(cp)
+        line["vs_comparator"] = value / cv if cv else None
     print(json.dumps(line), flush=True)
 
 

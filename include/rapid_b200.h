@@ -179,6 +179,12 @@ typedef struct {
   void* attn_ws;
   size_t attn_ws_bytes;
   void* tp;  /* this phase's TP context from rb_tp_create (NULL: single GPU) */
+  /* in-situ roofline probe (bench.py): when both are non-NULL, cudaEvent_t handles (timing
+   * enabled) recorded on the stream right before and after layer probe_layer's decode
+   * attention launch; captured as event-record nodes when the call is graph-captured. */
+  void* probe_ev0;
+  void* probe_ev1;
+  int probe_layer;
 } rb_workspace_t;
 
 typedef struct {

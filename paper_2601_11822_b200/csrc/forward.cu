@@ -47,6 +47,17 @@ extern "C" int rb_set_decode_glu(int on) {
   return 0;
 }
 
+// An event record that survives stream capture: inside a capture it must be an external
+// event-record node (a plain record would become a graph-internal dependency).
+static int record_event(void* ev, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) return rb::set_error("probe: cudaStreamIsCapturing failed");
+  const unsigned flags = cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+  if (cudaEventRecordWithFlags(reinterpret_cast<cudaEvent_t>(ev), st, flags) != cudaSuccess)
+    return rb::set_error("probe: cudaEventRecordWithFlags failed");
+  return 0;
+}
+
 #define RB_TRY(x)          \
   do {                     \
     int _rc = (x);         \
@@ -97,10 +108,14 @@ extern "C" int rb_decoder_forward(const rb_model_t* m, const rb_workspace_t* w, 
       RB_TRY(rope_cache_launch(qkv, nq, w->pos, w->slot, m->block_table, m->bt_stride, m->cos_sin, q, Hq * D, cache,
                                T, Hq, Hkv, D, st));
     }
-    if (nd > 0)
+    if (nd > 0) {
+      const bool probe = w->probe_ev0 && w->probe_ev1 && l == w->probe_layer;
+      if (probe) RB_TRY(record_event(w->probe_ev0, st));
       RB_TRY(decode_attention_launch(q, (long long)Hq * D, cache, m->block_table, m->bt_stride, w->slot, w->seq, attn,
                                      (long long)Hq * D, w->attn_ws, w->attn_ws_bytes, nd, Hq, Hkv, D, b->max_pages,
                                      m->attn_scale, m->num_blocks, sms, st));
+      if (probe) RB_TRY(record_event(w->probe_ev1, st));
+    }
     if (np > 0)
       RB_TRY(prefill_attention_tc_launch(q + (size_t)nd * Hq * D * e, (long long)Hq * D, cache,
                                          m->block_table + (size_t)b->prefill_slot * m->bt_stride, np,

@@ -145,3 +145,63 @@ class ReplayExecutor(CostModelExecutor):
 
     def exhausted(self) -> bool:
         return not self.q["prefill"] and not self.q["decode"]
+
+
+class MeasuredTableExecutor(CostModelExecutor):
+    """Device = the B200 tables profiler.py MEASURED (arm.MeasuredProfile), on the virtual
+    clock: a decode step of batch B on a D-SM partition costs the measured contended step
+    (linear between the measured batches), a prefill chunk costs its tokens x the measured
+    per-token time of the complementary partition; OVERALLOCATE with both phases busy costs
+    the measured OVERALLOCATE pair, and a phase running alone gets the whole device (decode:
+    the widest measured partition; prefill: the measured full-device rate). Used to tune ARM
+    policies on the CPU before spending GPU time (scripts/arm_sim.py); not a parity path."""
+
+    def __init__(self, mp, num_blocks: int | None = None, block_size: int = 16):
+        self.mp = mp
+        self.num_blocks = num_blocks
+        self.block_size = block_size
+        self._alone_pre = float(mp.data.get("full_prefill_alone_us_per_token", mp.prefill_us_per_token(None)))
+
+    def make_pool(self, model, gpu):
+        from paper_2601_11822_b200.blockpool import BlockPool
+
+        if self.num_blocks is None:
+            return BlockPool.for_device(model, gpu, name="gpu0")
+        return BlockPool(self.num_blocks, self.block_size, name="gpu0")
+
+    def _dec(self, d, b: int) -> float:
+        bs = self.mp.batches
+        b = max(1, b)
+        if b >= bs[-1]:
+            return self.mp.decode_us(d, bs[-1]) * b / bs[-1]
+        hi = next(x for x in bs if x >= b)
+        lo = max((x for x in bs if x <= b), default=hi)
+        t_hi = self.mp.decode_us(d, hi)
+        if hi == lo:
+            return t_hi
+        t_lo = self.mp.decode_us(d, lo)
+        return t_lo + (t_hi - t_lo) * (b - lo) / (hi - lo)
+
+    def _split(self, decision):
+        if decision.mode is AllocationMode.OVERALLOCATE:
+            return None
+        return round(decision.cu_fraction_decode * self.mp.total)
+
+    def launch_prefill(self, req, written, chunk, target, decision, co_decode) -> PricedHandle:
+        d = self._split(decision)
+        if d is None and co_decode is None:
+            us = chunk * self._alone_pre
+        else:
+            us = chunk * self.mp.prefill_us_per_token(d, co_decode[0] if co_decode else None)
+        cu = decision.cu_fraction_prefill if d is not None else 1.0
+        return PricedHandle(max(1, int(round(us))), cu, "prefill")
+
+    def launch_decode(self, members, decision, co_prefill_chunk) -> PricedHandle:
+        d = self._split(decision)
+        b = len(members)
+        if d is None and co_prefill_chunk is None:
+            us = self._dec(self.mp.ladder[-1], b)
+        else:
+            us = self._dec(d, b)
+        cu = decision.cu_fraction_decode if d is not None else 1.0
+        return PricedHandle(max(1, int(round(us))), cu, "decode", tuple(members))

@@ -79,7 +79,7 @@ class B200Executor:
                  num_blocks: int | None = None, kv_memory_fraction: float = 0.90, max_context: int | None = None,
                  num_slots: int = 1024, device: str = "cuda", token_source=None, use_graphs: bool = True,
                  batch_grid: tuple[int, ...] = DEFAULT_BATCH_GRID, serialize_phases: bool = False,
-                 record_logits: bool = False):
+                 record_logits: bool = False, probe_attention: bool = False):
         self.arch = arch
         dev = torch.device(device)
         self.device = dev if dev.index is not None else torch.device("cuda", torch.cuda.current_device())
@@ -148,6 +148,13 @@ class B200Executor:
         self.lazy_captures = 0
         self.step_log: list[tuple[int, int, int]] = []  # (B, gpu_us, host launch ns)
         self.prefill_log: list[tuple[int, int]] = []  # (gpu_us, host launch ns)
+        # in-situ decode-attention roofline: (algorithmic K+V bytes, kernel ms, decode SMs, host
+        # launch ns) of the probed layer in every decode step (CUDA events inside the graphs)
+        self.attn_probe_log: list[tuple[int, float, int, int]] = []
+        self._probe_events = None
+        if probe_attention:
+            self._probe_events = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            self.runner.set_attention_probe(*self._probe_events, layer=arch.layers // 2)
 
     # ------------------------------------------------------------------ sizing
     def _activation_bytes(self, T: int, B: int) -> int:
@@ -399,6 +406,9 @@ class B200Executor:
         h.finish_record(part.ds)
         h.members = tuple(members)
         h.lame = lame
+        h.d_sms = part.d_sms
+        # K+V bytes the probed layer's attention reads: every row's context (bf16)
+        h.attn_bytes = sum(seq) * self.arch.kv_heads * self.arch.head_dim * 4
         self.decode_steps += 1
         return h
 
@@ -413,6 +423,10 @@ class B200Executor:
                 if rows is not None:
                     self.logits.setdefault(r.id, []).append(rows[i])
         self.step_log.append((len(handle.members), handle.gpu_us, handle.launch_ns))
+        if self._probe_events is not None:
+            # the step's end event has completed, so this step's probe records are final
+            self.attn_probe_log.append((handle.attn_bytes, self._probe_events[0].elapsed_time(self._probe_events[1]),
+                                        handle.d_sms, handle.launch_ns))
 
     # ------------------------------------------------------------------ hybrid (K9 fused iteration)
     def launch_hybrid(self, members, head, written, chunk, target):

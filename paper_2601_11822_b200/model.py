@@ -208,10 +208,22 @@ class Runner:
         self.max_decode_batch = max_decode_batch
         self.scale = 1.0 / math.sqrt(arch.head_dim)
         self.eps = arch.rms_eps
+        # in-situ roofline probe of decode attention: {"probe_ev0", "probe_ev1", "probe_layer"}
+        # (raw cudaEvent_t handles), see set_attention_probe
+        self.probe: dict | None = None
         chunks = max(1, (max_blocks_per_seq + 7) // 8)  # decode attention splits <= ceil(pages / 8)
         self.attn_ws = torch.zeros(max_decode_batch * arch.q_heads * chunks * (arch.head_dim + 2),
                                    dtype=torch.float32,
                                    device=self.device)
+
+    def set_attention_probe(self, ev0: torch.cuda.Event, ev1: torch.cuda.Event, layer: int) -> None:
+        """Record ev0/ev1 around layer `layer`'s decode attention in every decode forward
+        (also inside captured graphs): the kernel's in-situ duration. Set before capture."""
+        for ev in (ev0, ev1):
+            if not ev.cuda_event:  # torch creates events lazily: force the handle into existence
+                ev.record()
+        torch.cuda.synchronize(self.device)
+        self.probe = {"probe_ev0": ev0.cuda_event, "probe_ev1": ev1.cuda_event, "probe_layer": int(layer)}
 
     @staticmethod
     def kv_bytes_per_block(arch: ArchConfig) -> int:
@@ -254,7 +266,8 @@ class Runner:
                                gemm_ws=B.scratch.ws.data_ptr(), gemm_ws_bytes=B.scratch.ws_bytes,
                                gemm_counters=B.scratch.counters.data_ptr(),
                                gemm_counters_len=B.scratch.counters.numel(), attn_ws=self.attn_ws.data_ptr(),
-                               attn_ws_bytes=self.attn_ws.numel() * 4, tp=B.tp.handle if B.tp is not None else None)
+                               attn_ws_bytes=self.attn_ws.numel() * 4, tp=B.tp.handle if B.tp is not None else None,
+                               **(self.probe if self.probe is not None and B is self.dec else {}))
 
     def kernels_per_forward(self, n_decode: int, n_prefill: int, logits_decode: bool, emit_prefill: bool,
                             sample: bool) -> int:

@@ -102,7 +102,8 @@ class RbWorkspace(ctypes.Structure):
     _fields_ = [(n, _vp) for n in ("x", "h", "qkv", "q", "attn", "gu", "act", "logits")] + [("rows_cap", _c_int)] + [
         (n, _vp) for n in ("ids", "pos", "slot", "seq", "out_ids")] + [
         ("gemm_ws", _vp), ("gemm_ws_bytes", _c_size), ("gemm_counters", _vp), ("gemm_counters_len", _c_int),
-        ("attn_ws", _vp), ("attn_ws_bytes", _c_size), ("tp", _vp)]
+        ("attn_ws", _vp), ("attn_ws_bytes", _c_size), ("tp", _vp), ("probe_ev0", _vp), ("probe_ev1", _vp),
+        ("probe_layer", _c_int)]
 
 
 class RbBatch(ctypes.Structure):

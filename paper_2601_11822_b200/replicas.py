@@ -44,3 +44,51 @@ def reduce_stats(local: ReplicaStats, group=None, device=None) -> dict:
     window, itl, ttft = float(m[0]), float(m[1]), float(m[2])
     return {"tokens": tokens, "finished": finished, "window_s": window, "tokens_per_s": tokens / window if window > 0
             else 0.0, "itl_p99_us": itl, "ttft_p50_us": ttft}
+
+
+def local_window_stats(requests, slo, horizon_us: int) -> dict:
+    """The per-replica ingredients of summarize() (slo.py, reference metrics.py:146-200)
+    that pool across replicas: in-window token stamps, finished-in-window counts, ITL gaps
+    and TTFTs of finished in-window requests."""
+    from paper_2601_11822_b200.slo import WARMUP_FRACTION, evaluate_request, itl_samples_us
+    from paper_2601_11822_b200.lifecycle import RequestState
+
+    cut = int(horizon_us * WARMUP_FRACTION)
+    finished = [r for r in requests if r.arrival_us >= cut and r.state is RequestState.FINISHED]
+    rows = [evaluate_request(r, slo) for r in finished]
+    return {
+        "stamps": sum(1 for r in requests for t in r.token_times_us if cut <= t <= horizon_us),
+        "finished": len(finished),
+        "ok_both": sum(1 for x in rows if x.meets_itl and x.meets_ttft),
+        "gaps": [g for r in finished for g in itl_samples_us(r)],
+        "ttfts": [x.ttft_us for x in rows if x.ttft_us >= 0],
+        "window_s": (horizon_us - cut) / 1e6,
+    }
+
+
+def pool_window_stats(local: dict, group=None) -> dict:
+    """Whole-job run-level metrics over all replicas: tokens/s = all in-window stamps / the
+    (common) window, p99 ITL / p50 TTFT nearest-rank over the POOLED samples of every replica
+    (not a max of per-rank percentiles). Every rank gets the result."""
+    import torch.distributed as dist
+
+    from paper_2601_11822_b200.slo import percentile_nearest_rank
+
+    parts = [local]
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        parts = [None] * dist.get_world_size(group)
+        dist.all_gather_object(parts, local, group=group)
+    window = max(p["window_s"] for p in parts)
+    gaps = [g for p in parts for g in p["gaps"]]
+    ttfts = [t for p in parts for t in p["ttfts"]]
+    return {
+        "replicas": len(parts),
+        "tokens_per_s": sum(p["stamps"] for p in parts) / window,
+        "per_replica_tokens_per_s": [p["stamps"] / p["window_s"] for p in parts],
+        "goodput": sum(p["ok_both"] for p in parts) / window,
+        "finished": sum(p["finished"] for p in parts),
+        "itl_p99_us": percentile_nearest_rank(gaps, 99.0) if gaps else 0.0,
+        "itl_p95_us": percentile_nearest_rank(gaps, 95.0) if gaps else 0.0,
+        "ttft_p50_us": percentile_nearest_rank(ttfts, 50.0) if ttfts else -1.0,
+        "window_s": window,
+    }

@@ -172,3 +172,47 @@ def test_committed_cost_fits():
             fit = json.load(fh)
         assert fit["partition_decode_rel_err"]["median"] < 0.1
         assert fit["overallocate_decode_rel_err"]["median"] < -0.3
+
+
+def test_feedback_policy_alternates_on_backlog():
+    """The backlog-buffered policy: prefill-heavy split while the ready-decoder backlog is
+    small, decode-heavy once it passes FB_BACKLOG_HI, back below FB_BACKLOG_LO (hysteresis);
+    both ends fit the SLO target at the batch cap and are pre-captured."""
+    mp = MeasuredProfile(synth())
+    arm = MeasuredArm(mp, 50_000, max_batch=256, policy="feedback")
+    lo, hi = arm._hull_pair(0.25)
+    assert lo <= hi
+    for d in (lo, hi):
+        assert mp.decode_us(d, 256) <= arm.target
+        assert d in arm.splits_used()
+    d0 = decode_sms_of(arm.decide(256, 2048, 0.25), 148)
+    assert d0 == lo
+    for _ in range(arm.FB_WINDOW):
+        arm.observe(20_000, 256, arm.FB_BACKLOG_HI, 3)
+    assert decode_sms_of(arm.decide(256, 2048, 0.25), 148) == hi
+    for _ in range(arm.FB_WINDOW):  # inside the hysteresis band: stays decode-heavy
+        arm.observe(20_000, 256, (arm.FB_BACKLOG_HI + arm.FB_BACKLOG_LO) // 2, 3)
+    assert decode_sms_of(arm.decide(256, 2048, 0.25), 148) == hi
+    for _ in range(arm.FB_WINDOW):
+        arm.observe(20_000, 256, 0, 3)
+    assert decode_sms_of(arm.decide(256, 2048, 0.25), 148) == lo
+    assert arm.decide(0, 100, 0.25).mode is AllocationMode.OVERALLOCATE
+
+
+def test_feedback_hull_beats_single_split_on_committed_profile():
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.dirname(__file__)), "profiles", "arm",
+                        "llama3.1-8b_ctx1152_chunk1023.json")
+    mp = MeasuredProfile.load(path)
+    arm = MeasuredArm(mp, 50_000, max_batch=256, policy="feedback")
+    lo, hi = arm._hull_pair(0.25)
+
+    def pt(d):
+        return 256 / mp.decode_us(d, 256), 0.25 / mp.prefill_us_per_token(d, 256)
+
+    (xl, yl), (xh, yh) = pt(lo), pt(hi)
+    a = (yl - xl) / ((yl - xl) + (xh - yh))
+    hull = xl + a * (xh - xl)
+    single = max(min(*pt(d)) for d in arm.candidates(256) if d is not None)
+    assert lo < hi and hull > single

@@ -150,12 +150,12 @@ def test_fixtures_present():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,compress,chunk,slo_us,num_blocks",
-                         [("cfg1_x50_chunk32_slo100us", 50, 32, 100, 1024),
+                         [("cfg1_x1000_chunk32_slo60us", 1000, 32, 60, 1024),
                           ("cfg1_x200_pool64_chunk32", 200, 32, 50_000, 64),
-                          ("cfg1_x50_chunk2048_slo100us", 50, 2048, 100, 1024)])
+                          ("cfg1_x1000_chunk2048_slo60us", 1000, 2048, 60, 1024)])
 def test_record_and_replay_gpu(name, compress, chunk, slo_us, num_blocks):
     """Serve the cfg-1 trace (time-compressed so batches form) on the B200 with the reference
-    ARM (allocate(); a 100 us SLO makes it PARTITION at batch >= 16, so launches move between
+    ARM (allocate(); a 60 us SLO makes it PARTITION whenever both phases have work, so launches move between
     green-context splits), record the timeline, replay it, compare."""
     from oracle.llama_fp32 import init_state
     from paper_2601_11822_b200.arm import CostParams
@@ -201,6 +201,6 @@ def test_record_and_replay_gpu(name, compress, chunk, slo_us, num_blocks):
     _check_ours(fx)
     if num_blocks == 64:
         assert fx["preemptions"] >= 1
-    if slo_us == 100:
+    if slo_us == 60:
         assert 0 < fx["partition_decisions"] < fx["decisions"], "want both OVERALLOCATE and PARTITION launches"
     ex.close()
