@@ -3,7 +3,10 @@ executor runs reaches the worker's executor in the same order with the same payl
 
 import os
 
-from paper_2601_11822_b200.tp_engine import CommandChannel, attach_leader, serve_worker, stop_workers
+import pytest
+
+from paper_2601_11822_b200.tp_engine import (CommandChannel, attach_leader, decode_command, encode_command,
+                                             serve_worker, stop_workers)
 
 
 class _RecordingExecutor:
@@ -36,26 +39,34 @@ def _commands():
     return out
 
 
-def _rank(rank, world, port, q):
+def _rank(rank, world, port, q, capacity):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    ch = CommandChannel()
+    ch = CommandChannel(capacity=capacity)
     ex = _RecordingExecutor()
     if rank == 0:
         attach_leader(ex, ch)
         for cmd in _commands():
             ex._issue(cmd)
         stop_workers(ch)
-        q.put((rank, ex.ran, ch.sent))
+        q.put((rank, ex.ran, ch.sent, ch.frames))
     else:
         n = serve_worker(ex, ch)
-        q.put((rank, ex.ran, n))
+        q.put((rank, ex.ran, n, ch.frames))
     dist.destroy_process_group()
 
 
-def test_leader_commands_replay_on_worker():
+def test_command_wire_format_round_trip():
+    for cmd in _commands() + [("prefill", 0, [], 3, [], 5, 7), ("stop",)]:
+        w = encode_command(cmd)
+        assert w.dtype.name == "int32" and int(w[0]) == w.shape[0]
+        assert decode_command(w) == cmd
+
+
+@pytest.mark.parametrize("capacity", [16384, 16])
+def test_leader_commands_replay_on_worker(capacity):
     import socket
 
     import torch.multiprocessing as mp
@@ -65,15 +76,20 @@ def test_leader_commands_replay_on_worker():
         port = s.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_rank, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, q, capacity)) for r in range(2)]
     for p in procs:
         p.start()
     out = sorted(q.get(timeout=120) for _ in procs)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    (_, leader_ran, sent), (_, worker_ran, n) = out
+    (_, leader_ran, sent, f0), (_, worker_ran, n, f1) = out
     want = _commands()
     assert leader_ran == want
     assert worker_ran == want
     assert n == len(want) and sent == len(want) + 1  # + STOP
+    assert f0 == f1  # every frame the leader broadcast was received
+    if capacity >= 16384:
+        assert f0 == sent  # one fixed-size frame per command
+    else:
+        assert f0 > sent  # long commands continued in further frames
