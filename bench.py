@@ -12,7 +12,8 @@ offline), one B200 per replica, synthetic trace `synthesize(WorkloadSpec(qps=Q*N
 duration_s=S, seed=42, mean_prompt_tokens=1024, mean_output_tokens=256, sigma=0))` with
 request i served by replica i mod N (replicas.shard_items), each replica the real-time RAPID
 engine (prefill and decode of different requests concurrently on disjoint SM partitions over
-one shared paged KV cache) with the measured adaptive ARM (profiles/arm/)
+one shared paged KV cache) with the measured ARM (profiles/arm/; default policy
+"balanced", tables re-measured in round 2 with both phases strictly under load)
 choosing the green-context split at every launch. `--decode-sms 72` runs cfg 2 (static
 green-context 50/50 split), `--arm` the reference cost-model allocate(), `--engine
 hybrid-2048` the same engine's chunked-prefill comparator as the primary arm.
@@ -62,7 +63,7 @@ sys.path.insert(0, ROOT)
 SLO_ITL_US = 50_000
 PROMPT, OUTPUT = 1024, 256
 # measured ARM tables (python -m paper_2601_11822_b200.profiler), per model, at its benchmark mix
-DEFAULT_PROFILES = {"llama3.1-8b": "llama3.1-8b_ctx1152_chunk1023.json", "qwen2.5-14b": "qwen2.5-14b_ctx8256.json"}
+DEFAULT_PROFILES = {"llama3.1-8b": "llama3.1-8b_ctx1152_chunk1023_r02.json", "qwen2.5-14b": "qwen2.5-14b_ctx8256.json"}
 
 
 def _peaks() -> dict:
@@ -221,19 +222,21 @@ def serve(args, arch, items, horizon, engine_kind, rank, world, local, *, primar
 
     hybrid = engine_kind.startswith("hybrid-")
     use_arm = args.arm or hybrid
+    # engine knob max_batch (config.py:263, default 256) per arm
+    mb = args.max_batch if primary else args.compare_max_batch
     max_ctx = PROMPT + OUTPUT + 64
     if hybrid:
         hchunk = int(engine_kind.split("-", 1)[1])
-        ex = HybridB200Executor(arch, seed=rank, max_batch=256, chunk_tokens=hchunk, max_context=max_ctx,
+        ex = HybridB200Executor(arch, seed=rank, max_batch=mb, chunk_tokens=hchunk, max_context=max_ctx,
                                 num_slots=4096)
     else:
-        ex = B200Executor(arch, seed=rank, static_decode_sms=None if args.arm else args.decode_sms, max_batch=256,
+        ex = B200Executor(arch, seed=rank, static_decode_sms=None if args.arm else args.decode_sms, max_batch=mb,
                           chunk_tokens=2048, max_context=max_ctx, num_slots=4096, probe_attention=True)
     policy = None
     if args.arm_profile and not hybrid:
         from paper_2601_11822_b200.arm import MeasuredArm, MeasuredProfile
 
-        policy = MeasuredArm(MeasuredProfile.load(args.arm_profile), SLO_ITL_US, 256, args.arm_policy)
+        policy = MeasuredArm(MeasuredProfile.load(args.arm_profile), SLO_ITL_US, mb, args.arm_policy)
         ex.warmup(sorted(policy.splits_used(), key=lambda d: -1 if d is None else d))
     else:
         ex.warmup()
@@ -242,7 +245,7 @@ def serve(args, arch, items, horizon, engine_kind, rank, world, local, *, primar
     model = arch.model_spec()
     slo = SloSpec(itl_slo_us=SLO_ITL_US)
     if hybrid:
-        engine = HybridEngine(model, b200_spec(), CostParams(), slo, chunk_tokens=hchunk, max_batch=256, executor=ex)
+        engine = HybridEngine(model, b200_spec(), CostParams(), slo, chunk_tokens=hchunk, max_batch=mb, executor=ex)
     else:
         part = ex._partitions[pkey]
         static = None if args.arm else AllocationDecision(AllocationMode.PARTITION, part.p_sms / total,
@@ -257,7 +260,7 @@ def serve(args, arch, items, horizon, engine_kind, rank, world, local, *, primar
                 fit = json.load(fh)
             gpu_spec = GpuSpec(**fit["gpu"])
             cost_params = dataclasses.replace(CostParams(), **fit["params"])
-        engine = RapidEngine(model, gpu_spec, cost_params, slo, chunk_tokens=2048, max_batch=256, executor=ex,
+        engine = RapidEngine(model, gpu_spec, cost_params, slo, chunk_tokens=2048, max_batch=mb, executor=ex,
                              static_decision=static, record_decisions=args.arm, arm_policy=policy)
 
     # ---- timed window over K decode steps, hooked on the executor
@@ -424,11 +427,13 @@ def main():
     ap.add_argument("--compare", default="auto",
                     help="second arm on the same trace in the same run: hybrid-<chunk> | none (auto: hybrid-2048 "
                          "when --engine rapid)")
+    ap.add_argument("--max-batch", type=int, default=256, help="engine max_batch of the primary arm (config.py:263)")
+    ap.add_argument("--compare-max-batch", type=int, default=256, help="max_batch of the hybrid comparator")
     ap.add_argument("--slo-ms", type=float, default=SLO_ITL_US / 1e3, help="p99 ITL SLO (default 50 ms)")
     ap.add_argument("--arm-profile", default="auto",
                     help="measured B200 ARM tables (profiler.py JSON; 'auto' = the committed profile of --model "
                          "under profiles/arm/)")
-    ap.add_argument("--arm-policy", default="adaptive", choices=["balanced", "slo-min", "adaptive", "feedback"])
+    ap.add_argument("--arm-policy", default="balanced", choices=["balanced", "slo-min", "adaptive", "feedback"])
     ap.add_argument("--arm", action="store_true",
                     help="the reference allocate() on the cost model instead of the measured ARM")
     ap.add_argument("--arm-calibrated", default=None,
@@ -539,7 +544,7 @@ def main():
         "dtype": "bf16",
         "data": f"synthetic (random-init {args.model} weights of the real shapes, synthesize() trace)",
         "config": {
-            "workload": (f"cfg3: {args.model} bf16, adaptive ARM ("
+            "workload": (f"cfg3: {args.model} bf16, measured ARM ("
                          + (f"measured B200 tables, {args.arm_policy} policy" if m["policy"] else
                             "reference allocate()")
                          + f" at every launch; OVERALLOCATE -> both phases on {m['total_sms']} SMs, PARTITION -> "
@@ -554,6 +559,7 @@ def main():
             "step": "one decode iteration (CUDA-graph replay); prefill runs concurrently on its partition"
                     if args.engine == "rapid" else "one fused hybrid iteration (decode rows + one prefill chunk)",
             "engine": args.engine,
+            "max_batch": args.max_batch,
         },
         "value_definition": ("reference summarize().tokens_per_s (metrics.py:146-200) over [10% horizon, horizon], "
                              "pooled over replicas (whole job); 0 when pooled p99 ITL > SLO"),
@@ -604,6 +610,7 @@ def main():
             "slo_met": bool(cp["itl_p99_us"] <= SLO_ITL_US), "goodput_req_s": cp["goodput"],
             "device_window_tokens_per_s": comp["tokens"] / (comp["ms"] / 1e3) if comp["complete"] else None,
             "mean_decode_batch": comp["mean_batch"], "run_wall_s": comp["run_wall_s"],
+            "max_batch": args.compare_max_batch,
             "note": "same trace, same engine code, same run; chunked-prefill hybrid batching on the whole device"}
         cv = constrained(cp)
         line["vs_comparator"] = value / cv if cv else None

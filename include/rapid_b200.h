@@ -48,6 +48,9 @@ int rb_debug_gemm_prefill_streamk(int on, double max_frac);
 /* Debug: token-major (prefill) GEMM tile width; 0 = wave-aware choice (default), else a forced
  * multiple of 32 in [32, 256]. Returns -1 for an invalid width. */
 int rb_debug_gemm_prefill_bn(int bn);
+/* Debug: query tiles per prefill-attention CTA; 0 = auto (default), 1, or 2 (mirrored causal
+ * pairs). Returns -1 for an invalid count. */
+int rb_debug_pattn_tiles(int tiles);
 /* Programmatic dependent launch for the forward's kernels (default on): each kernel may
  * start its prologue while its predecessor in the stream drains. 0 = plain serialization. */
 int rb_set_pdl(int on);

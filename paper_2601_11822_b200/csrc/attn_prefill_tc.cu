@@ -90,10 +90,10 @@ __device__ __forceinline__ void tmem_ld_x32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// kTiles query tiles per CTA (same head, consecutive 128-row tiles, one softmax warpgroup
-// each): every K/V tile is loaded once for both, and two warpgroups run softmax while the
-// tensor cores work on the other tile. The earlier tile of a pair needs fewer key tiles
-// (causal); its MMAs simply stop there.
+// kTiles query tiles per CTA (same head, one softmax warpgroup each; two = the mirrored
+// causal pair g, nqb-1-g): every K/V tile is loaded once for both, and two warpgroups run
+// softmax while the tensor cores work on the other tile. The short tile of a pair needs
+// fewer key tiles (causal); its MMAs simply stop there.
 template <int kTiles>
 __global__ void __launch_bounds__(64 + 128 * kTiles, 1)
     prefill_attn_tc_kernel(const __grid_constant__ CUtensorMap q_map, const __grid_constant__ CUtensorMap kv_map,
@@ -122,15 +122,25 @@ __global__ void __launch_bounds__(64 + 128 * kTiles, 1)
   const int lane = threadIdx.x & 31;
   const int nqb = (T + kBMq - 1) / kBMq;
   const int ngroups = (nqb + kTiles - 1) / kTiles;
-  const int grp = ngroups - 1 - (int)blockIdx.x;  // latest (heaviest) query tiles first
   const int hq = blockIdx.y;
   const int hk = hq / (Hq / Hkv);
   const int chunk_end = start + T;
   const int last_page = (chunk_end - 1) / kPage;  // highest page index this chunk may touch
-  int ntile[kTiles];                               // key tiles of each query tile (0: no such tile)
+  // Query tiles of this CTA. One tile: latest (heaviest) first. Two: mirrored pairs
+  // (g, nqb-1-g), so every CTA of a causal chunk carries the same number of key tiles
+  // (the short tile's keys are a prefix of the long one's: its MMAs stop early).
+  int qtile[kTiles];
+  int ntile[kTiles];  // key tiles of each query tile (0: no such tile)
+  if (kTiles == 1) {
+    qtile[0] = ngroups - 1 - (int)blockIdx.x;
+  } else {
+    const int gsel = (int)blockIdx.x;
+    qtile[0] = nqb - 1 - gsel;               // the long tile first (warpgroup 0)
+    qtile[kTiles - 1] = gsel < nqb - 1 - gsel ? gsel : nqb;  // middle of an odd count: alone
+  }
 #pragma unroll
   for (int w = 0; w < kTiles; ++w) {
-    const int qb = grp * kTiles + w;
+    const int qb = qtile[w];
     const int kv_end = start + min(T, qb * kBMq + kBMq);
     ntile[w] = qb < nqb ? (kv_end + kBN - 1) / kBN : 0;
   }
@@ -174,7 +184,7 @@ __global__ void __launch_bounds__(64 + 128 * kTiles, 1)
 #pragma unroll
       for (int w = 0; w < kTiles; ++w) {
         if (ntile[w] == 0) continue;
-        const int q0 = (grp * kTiles + w) * kBMq;
+        const int q0 = qtile[w] * kBMq;
         tma_load_3d(sQ + w * kQBytes, &q_map, q_full, 0, hq, q0);
         tma_load_3d(sQ + w * kQBytes + kQBytes / 2, &q_map, q_full, 64, hq, q0);
       }
@@ -257,7 +267,7 @@ __global__ void __launch_bounds__(64 + 128 * kTiles, 1)
     const int w = (warp - 2) >> 2;
     const int qd = warp & 3;
     const int row = qd * 32 + lane;
-    const int q0 = (grp * kTiles + w) * kBMq;
+    const int q0 = qtile[w] * kBMq;
     const int qpos = start + q0 + row;
     const int kv_end = start + min(T, q0 + kBMq);
     const int nt = ntile[w];
@@ -406,6 +416,13 @@ typedef CUresult (*PFN_encodeTiled3)(CUtensorMap*, CUtensorMapDataType, cuuint32
                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
+static int g_pattn_tiles = 0;  // debug override: 0 auto, 1 or 2 query tiles per CTA
+int prefill_attn_set_tiles(int tiles) {
+  if (tiles < 0 || tiles > 2) return -1;
+  g_pattn_tiles = tiles;
+  return 0;
+}
+
 int prefill_attention_tc_launch(const void* q, long long q_tok_stride, const void* cache_layer, const int* bt, int T,
                                 int start, int Hq, int Hkv, int head_dim, void* out, long long out_tok_stride,
                                 float scale, int num_blocks, cudaStream_t st) {
@@ -433,12 +450,14 @@ int prefill_attention_tc_launch(const void* q, long long q_tok_stride, const voi
   CUtensorMap kvmap;
   int rc = make_tmap_2d_bf16(&kvmap, cache_layer, kD, (uint64_t)num_blocks * 2 * Hkv * kPage, kD, 64, kPage);
   if (rc) return rc;
-  // two query tiles per CTA (shared K/V tiles, two softmax warpgroups) where the pair is
-  // balanced or the grid is small: a long paged prefix (both tiles see ~the same keys) or
-  // <= 8 query tiles; long causal chunks from position 0 keep one tile per CTA (measured:
-  // T=1023 32.7 vs 35.2 us, 2048 after 6144 387 vs 403 us, T=2048 from 0 93 vs 86 us)
+  // two query tiles per CTA (mirrored causal pairs sharing every K/V tile, two softmax
+  // warpgroups) unless that leaves too few CTAs to fill the GPU. Measured on 148 SMs
+  // (Llama-8B heads, profiles/r02/pattn/): T=1023 from 0 23.6 us (1 tile: 33.3), T=2048 from
+  // 0 71.2 (82.8), 2048 after 6144 363 (394), 1023 after 1024 48.3 (60.2); T=512 (64 pair
+  // CTAs) 15.5 vs 13.3 with one tile per CTA.
   const int nqb = (T + kBMq - 1) / kBMq;
-  const int tiles = (nqb >= 2 && (start >= T || nqb <= 8)) ? 2 : 1;
+  int tiles = (nqb >= 2 && ((nqb + 1) / 2) * Hq >= 96) ? 2 : 1;
+  if (g_pattn_tiles == 1 || (g_pattn_tiles == 2 && nqb >= 2)) tiles = g_pattn_tiles;
   const int smem = tiles * (kQBytes + 2 * kPBytes) + kStages * kKVStage + (2 * kStages + 1 + 10 * tiles) * 8 + 16 +
                    1024;
   using Fn = void (*)(const CUtensorMap, const CUtensorMap, const int*, int, int, int, int, __nv_bfloat16*, long long,

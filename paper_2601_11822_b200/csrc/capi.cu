@@ -29,6 +29,7 @@ int gemm_set_pair_mode(int mode);
 int gemm_set_variant(int v);
 int gemm_set_prefill_streamk(int on, double max_frac);
 int gemm_set_prefill_bn(int bn);
+int prefill_attn_set_tiles(int tiles);
 }  // namespace rb
 
 #define ST(s) reinterpret_cast<cudaStream_t>(s)
@@ -43,6 +44,7 @@ int rb_debug_gemm_pair_mode(int mode) { return rb::gemm_set_pair_mode(mode); }
 int rb_debug_gemm_variant(int v) { return rb::gemm_set_variant(v); }
 int rb_debug_gemm_prefill_streamk(int on, double max_frac) { return rb::gemm_set_prefill_streamk(on, max_frac); }
 int rb_debug_gemm_prefill_bn(int bn) { return rb::gemm_set_prefill_bn(bn); }
+int rb_debug_pattn_tiles(int tiles) { return rb::prefill_attn_set_tiles(tiles); }
 int rb_set_pdl(int on) {
   rb::set_pdl(on != 0);
   return 0;

@@ -91,6 +91,8 @@ class B200Executor:
         self.num_slots = num_slots
         self.use_graphs = use_graphs
         self.grid = tuple(b for b in batch_grid if b <= max_batch) or (max_batch,)
+        # batches past the grid's last entry (max_batch > 256) get 32-row buckets, not one pad to max_batch
+        self.grid = self.grid + tuple(range(self.grid[-1] + 32, max_batch, 32))
         if self.grid[-1] < max_batch:
             self.grid = self.grid + (max_batch,)
         self.total_sms = ops.device_sm_count(self.device.index or 0)

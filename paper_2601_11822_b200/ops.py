@@ -34,6 +34,7 @@ _SIGS = {
     "rb_debug_gemm_variant": ([_c_int], _c_int),
     "rb_debug_gemm_prefill_streamk": ([_c_int, ctypes.c_double], _c_int),
     "rb_debug_gemm_prefill_bn": ([_c_int], _c_int),
+    "rb_debug_pattn_tiles": ([_c_int], _c_int),
     "rb_set_pdl": ([_c_int], _c_int),
     "rb_set_decode_glu": ([_c_int], _c_int),
     "rb_gemm_bf16": (

@@ -98,25 +98,43 @@ def measure(model: str = "llama3.1-8b", ctx: int = 1152, chunk: int = 2048, ladd
             g.replay()
             ds.synchronize()
             dts = []
+            est = 20_000.0
             for _ in range(reps):
                 torch.cuda.synchronize()
-                # keep the prefill partition busy for the whole decode window: chunks are
-                # queued first; the decode events bracket replays that start once it runs
-                n_chunks = 1 + int(steps * (dts[-1] if dts else 20_000.0) * 1.5 / max(p_alone, 1.0))
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(ps)
-                for _ in range(min(n_chunks, 16)):
+                # Both sides under load: prefill chunks and decode replays are queued on their
+                # streams together, each bracketed by events; a decode step counts only if it ran
+                # entirely while prefill chunks were running, and a chunk only if it ran entirely
+                # inside the decode replays (an earlier version timed chunks that outlived the
+                # decode window, under-stating the contention by 15-22%: profiles/r02/arm/).
+                n_chunks = max(4, min(16, 1 + int(steps * est * 1.5 / max(p_alone, 1.0))))
+                n_dec = max(steps, min(64, 2 + int(n_chunks * p_alone * 1.2 / max(est, 1.0))))
+                ref = torch.cuda.Event(enable_timing=True)
+                ref.record(ps)
+                ds.wait_event(ref)
+                pev, dev = [], []
+                for _ in range(n_chunks):
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(ps)
                     prefill_chunk()
-                b.record(ps)
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    b.record(ps)
+                    pev.append((a, b))
                 with torch.cuda.stream(ds):
-                    e0.record(ds)
-                    for _ in range(steps):
+                    for _ in range(n_dec):
+                        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        a.record(ds)
                         g.replay()
-                    e1.record(ds)
+                        b.record(ds)
+                        dev.append((a, b))
                 torch.cuda.synchronize()
-                dts.append(e0.elapsed_time(e1) * 1e3 / steps)
-                pre_conc.append(a.elapsed_time(b) * 1e3 / min(n_chunks, 16))
+                P = [(ref.elapsed_time(a) * 1e3, ref.elapsed_time(b) * 1e3) for a, b in pev]
+                D = [(ref.elapsed_time(a) * 1e3, ref.elapsed_time(b) * 1e3) for a, b in dev]
+                d_in = [e - s0 for s0, e in D if s0 >= P[0][0] and e <= P[-1][1]]
+                p_in = [e - s0 for s0, e in P if s0 >= D[0][0] and e <= D[-1][1]]
+                d_in = d_in or [e - s0 for s0, e in D]
+                p_in = p_in or [e - s0 for s0, e in P]
+                dts.append(_med(d_in))
+                est = dts[-1]
+                pre_conc.append(_med(p_in))
             dec[B] = round(_med(dts), 1)
             pre_by_b[B] = round(_med(pre_conc[-reps:]) / chunk, 3)
             del g

@@ -1,4 +1,9 @@
-"""Prefill attention (K2 tcgen05) time for one chunk: T tokens after a prefix, Llama-8B heads."""
+"""Prefill attention (K2 tcgen05) time for one chunk: T tokens after a prefix, Llama-8B heads,
+for each CTA shape (auto / one query tile / mirrored pair of tiles).
+
+    python scripts/pattn_bench.py [--tiles 0,1,2]
+"""
+import argparse
 import json
 import os
 import sys
@@ -8,24 +13,35 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2601_11822_b200 import ops  # noqa: E402
 
-ops.load()
-Hq, Hkv, D = 32, 8, 128
-for T, start in [(1023, 0), (2048, 0), (2048, 6144)]:
+ap = argparse.ArgumentParser()
+ap.add_argument("--tiles", default="0,1,2")
+ap.add_argument("--cases", default="1023:0,2048:0,2048:6144,512:0,1023:1024")
+ap.add_argument("--hq", type=int, default=32)
+ap.add_argument("--hkv", type=int, default=8)
+args = ap.parse_args()
+lib = ops.load()
+Hq, Hkv, D = args.hq, args.hkv, 128
+for case in args.cases.split(","):
+    T, start = (int(x) for x in case.split(":"))
     n = start + T
     npg = (n + 15) // 16
     cache = torch.randn(npg + 8, 2, Hkv, 16, D, device="cuda").bfloat16()
     bt = torch.arange(npg, dtype=torch.int32, device="cuda")
     q = torch.randn(T, Hq, D, device="cuda").bfloat16()
     out = torch.empty_like(q)
-    for _ in range(2):
-        ops.prefill_attention(q, cache, bt, start, out, num_kv_heads=Hkv)
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(10):
-        ops.prefill_attention(q, cache, bt, start, out, num_kv_heads=Hkv)
-    b.record()
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / 10
-    fl = 4 * Hq * D * (T * T / 2 + T * start)
-    print(json.dumps({"T": T, "start": start, "us": round(ms * 1e3, 1), "tflops": round(fl / ms / 1e9, 1)}))
+    for tiles in (int(t) for t in args.tiles.split(",")):
+        lib.rb_debug_pattn_tiles(tiles)
+        for _ in range(2):
+            ops.prefill_attention(q, cache, bt, start, out, num_kv_heads=Hkv)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(20):
+            ops.prefill_attention(q, cache, bt, start, out, num_kv_heads=Hkv)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / 20
+        fl = 4 * Hq * D * (T * T / 2 + T * start)
+        print(json.dumps({"T": T, "start": start, "tiles": tiles, "us": round(ms * 1e3, 1),
+                          "tflops": round(fl / ms / 1e9, 1)}), flush=True)
+    lib.rb_debug_pattn_tiles(0)

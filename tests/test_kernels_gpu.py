@@ -242,6 +242,28 @@ def test_prefill_attention(T, start, Hq, Hkv):
     assert rel_l2(out, ref) < 1e-2
 
 
+@pytest.mark.parametrize("tiles", [1, 2])
+@pytest.mark.parametrize("T,start", [(1100, 0), (1023, 0), (640, 0), (129, 0), (700, 900)])
+def test_prefill_attention_forced_tiles(T, start, tiles):
+    """Both CTA shapes on every chunk shape: one query tile per CTA, or mirrored causal pairs
+    (g, nqb-1-g) — odd tile counts leave the middle tile alone in its CTA."""
+    lib = ops.load()
+    gen = torch.Generator(device=DEV).manual_seed(3 * T + start + tiles)
+    D, nb, Hq, Hkv = 128, 256, 8, 2
+    cache = _make_cache(nb, Hkv, D, gen)
+    bt_row = torch.randperm(nb, device=DEV, generator=gen).int()[:160].contiguous()
+    q = torch.randn(T, Hq, D, device=DEV, generator=gen).bfloat16()
+    out = torch.empty(T, Hq, D, device=DEV, dtype=torch.bfloat16)
+    assert lib.rb_debug_pattn_tiles(tiles) == 0
+    try:
+        ops.prefill_attention(q, cache, bt_row, start, out, num_kv_heads=Hkv)
+        torch.cuda.synchronize()
+    finally:
+        lib.rb_debug_pattn_tiles(0)
+    k, v = _gather_kv(cache, bt_row, start + T)
+    assert rel_l2(out, _ref_attn(q, k, v, causal_offset=start)) < 1e-2
+
+
 @pytest.mark.parametrize("T,start", [(300, 0), (200, 333)])
 def test_prefill_attention_growing_max(T, start):
     """Scores that grow along the keys force the tcgen05 kernel's lazy O rescale (row max
