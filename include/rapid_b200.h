@@ -51,6 +51,21 @@ int rb_debug_gemm_prefill_bn(int bn);
 /* Debug: query tiles per prefill-attention CTA; 0 = auto (default), 1, or 2 (mirrored causal
  * pairs). Returns -1 for an invalid count. */
 int rb_debug_pattn_tiles(int tiles);
+/* Debug: decode attention page loads, 1 = one 5D TMA op per page and kv-head (default), 0 = four
+ * 2D {64, 16} boxes. */
+int rb_debug_decode_kv_one_op(int on);
+/* Debug: decode attention ring shape, 0 = auto (default), 1..4 = 12x2, 8x3, 6x4, 4x6
+ * (warps per CTA x smem stages per warp). Returns -1 for an invalid shape. */
+int rb_debug_decode_attn_shape(int shape);
+/* Debug (diagnostic, csrc/probe.cu): stream `bytes` of global memory into shared memory with
+ * 1D bulk copies over a ring of `stages` x `chunk` bytes, one CTA per SM, no compute — the
+ * per-SM ingest ceiling of a partition. `sink` is a device int the kernel may write. */
+int rb_debug_stream_read(const void* src, long long bytes, int chunk, int stages, int num_sms, int* sink,
+                         void* stream);
+/* Debug: the same with 2D tensor-TMA boxes {64 bf16, box_rows} (128B swizzle), per_stage boxes
+ * per ring stage. */
+int rb_debug_stream_read_tma(const void* src, long long bytes, int box_rows, int per_stage, int stages, int num_sms,
+                             int* sink, void* stream);
 /* Programmatic dependent launch for the forward's kernels (default on): each kernel may
  * start its prologue while its predecessor in the stream drains. 0 = plain serialization. */
 int rb_set_pdl(int on);

@@ -37,6 +37,7 @@ constexpr int kPage = 16;
 // partitions, where more warps in flight per SM measured up to +35% (56 SMs, B=226)
 constexpr int kStageBytes = 4 * 2048;     // K lo/hi + V lo/hi, 16 rows x 128 B each
 constexpr int kPStageBytes = 256;         // P^T staging per warp
+constexpr float kLazyLog2 = 8.0f;         // stale-max slack of the online softmax (P <= 2^8)
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -77,6 +78,7 @@ struct DecArgs {
   int B, Hkv, G, splits, chunk_pages;
   float scale_log2;
   int* work;  // [2] self-resetting (next item, finished warps): dynamic item assignment; null = static
+  int one_op;  // 1: kv_map is the 5D page map (one 8 KB TMA op per page); 0: 2D rows (four 2 KB boxes)
 };
 
 constexpr int kQueue = 8;  // per-warp ring of acquired item ids (producer lane 0 -> all lanes)
@@ -131,11 +133,18 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   int qtail = 0;
   auto next_item = [&](int cur) { return a.work ? atomicAdd(&a.work[0], 1) : cur + nw; };
   int pi = a.work ? -1 : gw, pp = 0, pp1 = 0, pb = 0, ph = 0, pc = 0, pn = 0;
+  // the block-table entry of the NEXT page to fetch is loaded one issue ahead (npage): the
+  // producer lane runs inside the consumer warp, so a dependent slot -> page load at issue
+  // time stalled the whole warp once per page (ncu: profiles/r02/dattn/)
+  const int* bt_row = nullptr;
+  int npage = 0;
   auto p_seek = [&]() {  // advance pi to an item with pages; sets pp..pp1 and enqueues it
     while (pi < total_items) {
       item_pages(a, pi, pb, ph, pc, pp, pp1, pn);
       if (pp < pp1) {
         queue[qtail++ & (kQueue - 1)] = pi;
+        bt_row = a.block_table + (size_t)a.row_slot[pb] * a.bt_stride;
+        npage = bt_row[pp];
         return;
       }
       pi = next_item(pi);
@@ -144,19 +153,26 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   };
   int issued = 0;
   auto p_issue = [&](int stage) {
-    const int slot = a.row_slot[pb];
-    const int page = a.block_table[(size_t)slot * a.bt_stride + pp];
+    const int page = npage;
     const int rowK = ((page * 2 + 0) * a.Hkv + ph) * kPage;
     const int rowV = ((page * 2 + 1) * a.Hkv + ph) * kPage;
     uint8_t* dst = ring + (size_t)stage * kStageBytes;
     mbar_arrive_expect_tx(&bars[stage], kStageBytes);
-    tma_load_2d(dst, &kv_map, &bars[stage], 0, rowK, kEvictFirst);
-    tma_load_2d(dst + 2048, &kv_map, &bars[stage], 64, rowK, kEvictFirst);
-    tma_load_2d(dst + 4096, &kv_map, &bars[stage], 0, rowV, kEvictFirst);
-    tma_load_2d(dst + 6144, &kv_map, &bars[stage], 64, rowV, kEvictFirst);
+    if (a.one_op) {
+      // the page's K and V halves of this head in one op (the per-op TMA cost, not bytes in
+      // flight, bounds small partitions: scripts/ingest_probe.py, profiles/r02/ingest/)
+      tma_load_5d(dst, &kv_map, &bars[stage], 0, 0, 0, 0, (page * 2) * a.Hkv + ph, kEvictFirst);
+    } else {
+      tma_load_2d(dst, &kv_map, &bars[stage], 0, rowK, kEvictFirst);
+      tma_load_2d(dst + 2048, &kv_map, &bars[stage], 64, rowK, kEvictFirst);
+      tma_load_2d(dst + 4096, &kv_map, &bars[stage], 0, rowV, kEvictFirst);
+      tma_load_2d(dst + 6144, &kv_map, &bars[stage], 64, rowV, kEvictFirst);
+    }
     if (++pp == pp1) {
       pi = next_item(pi);
       p_seek();
+    } else {
+      npage = bt_row[pp];  // consumed at the next issue, a page of math later
     }
   };
   if (lane == 0) {
@@ -198,20 +214,21 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       const uint32_t base = smem_u32(ring + (size_t)stage * kStageBytes);
       // ---- S^T = K Q^T: even / odd k-steps into two accumulators (halves the MMA
       // dependency chain on the critical path of every page)
-      float s[4] = {0.f, 0.f, 0.f, 0.f};
-      float s2[4] = {0.f, 0.f, 0.f, 0.f};
+      // (four accumulators over the 8 k-steps: a dependent chain of 2 MMAs, not 8)
+      float sa[4][4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) sa[c][0] = sa[c][1] = sa[c][2] = sa[c][3] = 0.f;
       const int mi = lane >> 3;
       const int rr = (mi & 1) * 8 + (lane & 7);
 #pragma unroll
-      for (int kk = 0; kk < 8; kk += 2) {
-        uint32_t a0, a1, a2, a3, c0, c1, c2, c3;
+      for (int kk = 0; kk < 8; ++kk) {
+        uint32_t a0, a1, a2, a3;
         ldsm_x4(base + pg_off(rr, 2 * kk + (mi >> 1)), a0, a1, a2, a3);
-        ldsm_x4(base + pg_off(rr, 2 * kk + 2 + (mi >> 1)), c0, c1, c2, c3);
-        mma_bf16_16816(s, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
-        mma_bf16_16816(s2, c0, c1, c2, c3, qb[kk + 1][0], qb[kk + 1][1]);
+        mma_bf16_16816(sa[kk & 3], a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
       }
+      float s[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) s[e] += s2[e];
+      for (int e = 0; e < 4; ++e) s[e] = (sa[0][e] + sa[1][e]) + (sa[2][e] + sa[3][e]);
       // ---- mask + online softmax (columns = heads 2t, 2t+1; rows = tokens g, g+8)
       const int tok0 = p * kPage + g;
       float s00 = s[0] * a.scale_log2, s01 = s[1] * a.scale_log2;
@@ -219,28 +236,36 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       if (tok0 >= n) { s00 = -FLT_MAX; s01 = -FLT_MAX; }
       if (tok0 + 8 >= n) { s10 = -FLT_MAX; s11 = -FLT_MAX; }
       float mx0 = fmaxf(s00, s10), mx1 = fmaxf(s01, s11);
+      // lazy max: the running (per-head, warp-uniform) max moves only when some score of the
+      // page exceeds it by more than 2^kLazyLog2 — otherwise P = 2^(s - m) <= 2^8 against the
+      // stale max (exact after the final 1/l) and the page skips the shuffle reduction, the
+      // alpha exp2 and the 32-register O rescale (the first page always takes the full path)
+      if (__any_sync(0xffffffffu, mx0 > m0 + kLazyLog2 || mx1 > m1 + kLazyLog2)) {
 #pragma unroll
-      for (int off = 4; off <= 16; off <<= 1) {
-        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
-        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
-      }
-      const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-      const float al0 = exp2f(m0 - mn0), al1 = exp2f(m1 - mn1);  // m0=-FLT_MAX first: exp2(-huge)=0
-      m0 = mn0;
-      m1 = mn1;
-      const float p00 = (s00 == -FLT_MAX) ? 0.f : exp2f(s00 - mn0);
-      const float p01 = (s01 == -FLT_MAX) ? 0.f : exp2f(s01 - mn1);
-      const float p10 = (s10 == -FLT_MAX) ? 0.f : exp2f(s10 - mn0);
-      const float p11 = (s11 == -FLT_MAX) ? 0.f : exp2f(s11 - mn1);
-      l0 = l0 * al0 + p00 + p10;
-      l1 = l1 * al1 + p01 + p11;
+        for (int off = 4; off <= 16; off <<= 1) {
+          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+        }
+        const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+        const float al0 = exp2f(m0 - mn0), al1 = exp2f(m1 - mn1);  // m0=-FLT_MAX first: exp2(-huge)=0
+        m0 = mn0;
+        m1 = mn1;
+        l0 *= al0;
+        l1 *= al1;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        o[i][0] *= al0;
-        o[i][1] *= al1;
-        o[i][2] *= al0;
-        o[i][3] *= al1;
+        for (int i = 0; i < 8; ++i) {
+          o[i][0] *= al0;
+          o[i][1] *= al1;
+          o[i][2] *= al0;
+          o[i][3] *= al1;
+        }
       }
+      const float p00 = (s00 == -FLT_MAX) ? 0.f : exp2f(s00 - m0);
+      const float p01 = (s01 == -FLT_MAX) ? 0.f : exp2f(s01 - m1);
+      const float p10 = (s10 == -FLT_MAX) ? 0.f : exp2f(s10 - m0);
+      const float p11 = (s11 == -FLT_MAX) ? 0.f : exp2f(s11 - m1);
+      l0 += p00 + p10;
+      l1 += p01 + p11;
       // ---- rows past the sequence end in the last page hold stale (possibly non-finite)
       // V; P is 0 there but 0 * NaN would still poison the MMA, so zero those rows.
       const int valid = n - p * kPage;
@@ -359,6 +384,18 @@ __global__ void decode_attn_combine_kernel(const float* __restrict__ part_o, con
   out[(size_t)b * out_tok_stride + (size_t)hq * kD + d] = __float2bfloat16_rn(l > 0.f ? o / l : 0.f);
 }
 
+static int g_decode_shape = 0;     // debug: ring shape override (0 = auto)
+int decode_attn_set_shape(int shape) {
+  if (shape < 0 || shape > 4) return -1;
+  g_decode_shape = shape;
+  return 0;
+}
+static int g_decode_kv_one_op = 1;  // 1: one 5D TMA op per page (default), 0: four 2D boxes
+int decode_attn_set_kv_ops(int one_op) {
+  g_decode_kv_one_op = one_op ? 1 : 0;
+  return 0;
+}
+
 int decode_attention_launch(const void* q, long long q_tok_stride, const void* cache_layer, const int* block_table,
                             int bt_stride, const int* row_slot, const int* seq_lens, void* out,
                             long long out_tok_stride, void* workspace, size_t ws_bytes, int B, int Hq, int Hkv,
@@ -374,8 +411,13 @@ int decode_attention_launch(const void* q, long long q_tok_stride, const void* c
   // partition at least one item (no partials, no combine pass); otherwise cut sequences into
   // chunks so there are ~4 items per warp (load balance for long contexts / small B).
   const bool small = num_sms <= 100;
-  const int kWarps = small ? 12 : 8;
-  const int kStages = small ? 2 : 3;
+  // ring shape (warps x stages per warp): auto 12 x 2 on <= 100-SM partitions, else 8 x 3;
+  // debug override g_decode_shape 1..4 = 12x2, 8x3, 6x4, 4x6
+  int shape = g_decode_shape ? g_decode_shape : (small ? 1 : 2);
+  static const int kShapeWarps[5] = {0, 12, 8, 6, 4};
+  static const int kShapeStages[5] = {0, 2, 3, 4, 6};
+  const int kWarps = kShapeWarps[shape];
+  const int kStages = kShapeStages[shape];
   const long long warps = (long long)num_sms * kWarps;
   const long long seqs = (long long)B * Hkv;
   int chunk_pages = max_pages;
@@ -422,18 +464,23 @@ int decode_attention_launch(const void* q, long long q_tok_stride, const void* c
     a.part_ml = a.part_o + items * G * kD;
   }
   CUtensorMap map;
-  const uint64_t rows = (uint64_t)num_blocks * 2 * Hkv * kPage;
-  int rc = make_tmap_2d_bf16(&map, cache_layer, kD, rows, kD, 64, kPage);
-  if (rc) return rc;
+  a.one_op = 0;
+  if (g_decode_kv_one_op && make_tmap_kv5d_bf16(&map, cache_layer, (uint64_t)num_blocks, Hkv) == 0) {
+    a.one_op = 1;
+  } else {
+    const uint64_t rows = (uint64_t)num_blocks * 2 * Hkv * kPage;
+    int rc = make_tmap_2d_bf16(&map, cache_layer, kD, rows, kD, 64, kPage);
+    if (rc) return rc;
+  }
   const int smem = kWarps * kStages * kStageBytes + kWarps * kPStageBytes + kWarps * kStages * 8 +
                    kWarps * kQueue * 4 + 1024;
   using Fn = void (*)(const CUtensorMap, const DecArgs);
-  const Fn kern = small ? decode_attn_tc_kernel<12, 2> : decode_attn_tc_kernel<8, 3>;
-  static bool attr[2] = {false, false};
-  if (!attr[small]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  static const Fn kerns[5] = {nullptr, decode_attn_tc_kernel<12, 2>, decode_attn_tc_kernel<8, 3>,
+                              decode_attn_tc_kernel<6, 4>, decode_attn_tc_kernel<4, 6>};
+  const Fn kern = kerns[shape];
+  {
+    cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(kern), 227 * 1024);
     if (e != cudaSuccess) return set_cuda_error("decode attn smem attr", e);
-    attr[small] = true;
   }
   const size_t warps_needed = items;
   int grid = (int)((warps_needed + kWarps - 1) / kWarps);

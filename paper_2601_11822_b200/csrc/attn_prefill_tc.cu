@@ -297,23 +297,22 @@ __global__ void __launch_bounds__(64 + 128 * kTiles, 1)
       const int kbase = j * kBN;
       // masked scores are -inf (exp2 -> 0 with no select); tile 0 always holds key 0 <= qpos,
       // so the max is finite from the first tile on. Only tiles crossing this row's diagonal
-      // or the chunk end need the per-key mask.
-      float mx = -INFINITY;
+      // or the chunk end need the per-key mask. The max runs on the raw scores (scale > 0)
+      // with four independent chains; the scale folds into the exponent's FFMA below.
+      float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
       if (kbase + kBN - 1 <= qpos && kbase + kBN <= kv_end) {
 #pragma unroll
-        for (int i = 0; i < kBN; ++i) {
-          s[i] *= scale_log2;
-          mx = fmaxf(mx, s[i]);
-        }
+        for (int i = 0; i < kBN; ++i) mq[i & 3] = fmaxf(mq[i & 3], s[i]);
       } else {
 #pragma unroll
         for (int i = 0; i < kBN; ++i) {
           const int kp = kbase + i;
-          const float v = (kp > qpos || kp >= kv_end) ? -INFINITY : s[i] * scale_log2;
+          const float v = (kp > qpos || kp >= kv_end) ? -INFINITY : s[i];
           s[i] = v;
-          mx = fmaxf(mx, v);
+          mq[i & 3] = fmaxf(mq[i & 3], v);
         }
       }
+      const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])) * scale_log2;
       // warp-uniform decision (tcgen05.ld/st below are warp-collective): when any row's stale
       // max is too far behind, every row of the warp moves its max up and rescales l and O
       if (__any_sync(0xffffffffu, mx > m + kRescaleLog2)) {
@@ -345,14 +344,15 @@ __global__ void __launch_bounds__(64 + 128 * kTiles, 1)
         }
         m = mn;
       }
-      float ps = 0.f;
+      float pq[4] = {0.f, 0.f, 0.f, 0.f};
+      const float neg_m = -m;
 #pragma unroll
       for (int i = 0; i < kBN; ++i) {
-        const float p = ex2_approx(s[i] - m);
+        const float p = ex2_approx(fmaf(s[i], scale_log2, neg_m));
         s[i] = p;
-        ps += p;
+        pq[i & 3] += p;
       }
-      l += ps;
+      l += (pq[0] + pq[1]) + (pq[2] + pq[3]);
       // P row -> smem (K-major SW128: row r at (r/8)*1024 + (r%8)*128, 16-B chunk c at c ^ (r%8))
       mbar_wait(&p_free[2 * w + b], ph2 ^ 1);
       uint8_t* prow = sP + (size_t)(2 * w + b) * kPBytes + (row >> 3) * 1024 + (row & 7) * 128;
@@ -463,11 +463,9 @@ int prefill_attention_tc_launch(const void* q, long long q_tok_stride, const voi
   using Fn = void (*)(const CUtensorMap, const CUtensorMap, const int*, int, int, int, int, __nv_bfloat16*, long long,
                       float);
   static const Fn fns[2] = {prefill_attn_tc_kernel<1>, prefill_attn_tc_kernel<2>};
-  static bool attr[2] = {false, false};
-  if (!attr[tiles - 1]) {
-    cudaError_t e = cudaFuncSetAttribute(fns[tiles - 1], cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  {
+    cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(fns[tiles - 1]), 227 * 1024);
     if (e != cudaSuccess) return set_cuda_error("prefill attn tc smem attr", e);
-    attr[tiles - 1] = true;
   }
   if (smem > 227 * 1024) return set_error("prefill attn tc: shared memory budget exceeded");
   dim3 grid((nqb + tiles - 1) / tiles, Hq);

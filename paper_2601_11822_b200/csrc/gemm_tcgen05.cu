@@ -978,14 +978,12 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
        {gemm_bf16_tcgen05_kernel<1, 2, 1>, gemm_bf16_tcgen05_kernel<1, 2, 2>}},
       {{gemm_bf16_tcgen05_kernel<2, 1, 1>, gemm_bf16_tcgen05_kernel<2, 1, 2>},
        {gemm_bf16_tcgen05_kernel<2, 2, 1>, gemm_bf16_tcgen05_kernel<2, 2, 2>}}};
-  static bool attr_done[2][2][2] = {};
   // decode epilogue sets: 2 (three warpgroups, setmaxnreg) except the MT=2 kernel at B <= 32
   const int sets = (swap && (MT == 1 || g_mt2_sets == 2 || (g_force_variant < 0 && BN > 32))) ? 2 : 1;
   const KernelFn kern = kernels[pair - 1][MT - 1][sets - 1];
-  if (!attr_done[pair - 1][MT - 1][sets - 1]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  {
+    cudaError_t e = set_smem_attr_once(reinterpret_cast<const void*>(kern), 227 * 1024);
     if (e != cudaSuccess) return set_cuda_error("gemm: set smem attr", e);
-    attr_done[pair - 1][MT - 1][sets - 1] = true;
   }
   cudaError_t e = launch_k(kern, dim3(pair * clusters), dim3(threads_for(sets)), smem, stream, pair, ta, tb, g);
   if (e != cudaSuccess) return set_cuda_error("gemm launch", e);

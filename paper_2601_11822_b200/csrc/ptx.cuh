@@ -326,6 +326,17 @@ __device__ __forceinline__ void tma_prefetch_l2_2d_w(const void* tmap, int32_t x
 
 // ---------------------------------------------------------------- PDL
 // Let the next kernel in the stream launch (its CTAs park in pdl_wait until we finish).
+// 5D tiled bulk tensor load (one paged-KV page of one head: csrc/rb_common.cu kv5d map)
+__device__ __forceinline__ void tma_load_5d(void* dst_smem, const void* tmap, uint64_t* bar, int32_t c0, int32_t c1,
+                                            int32_t c2, int32_t c3, int32_t c4, uint64_t hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(dst_smem)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+      "l"(hint)
+      : "memory");
+}
+
 // 1D bulk copy global -> this CTA's smem, completion counted on `bar` (bytes % 16 == 0)
 __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"

@@ -3,6 +3,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <set>
 #include <unordered_map>
 
 namespace rb {
@@ -101,4 +102,58 @@ static bool g_pdl = true;
 bool pdl_enabled() { return g_pdl; }
 void set_pdl(bool on) { g_pdl = on; }
 
+}  // namespace rb
+
+namespace rb {
+// Paged KV cache layer [nb][2 (K,V)][Hkv][16][128] bf16 as a 5D tensor for one-op-per-page
+// loads: d0 = 64 dims (128 B, swizzled), d1 = 16 tokens (256 B), d2 = 2 dim halves (128 B),
+// d3 = K/V (Hkv x 4 KB), d4 = 4 KB page-head rows ((page * 2 + kv) * Hkv + head). A box
+// {64, 16, 2, 2, 1} lands as [K lo | K hi | V lo | V hi] x 16 rows x 128 B, the same smem
+// image as four {64, 16} boxes of the 2D view.
+int make_tmap_kv5d_bf16(CUtensorMap* map, const void* cache_layer, uint64_t num_blocks, int hkv) {
+  static std::mutex mu;
+  static std::unordered_map<TmapKey, CUtensorMap, TmapKeyHash> cache;
+  TmapKey key{reinterpret_cast<uint64_t>(cache_layer), num_blocks, (uint64_t)hkv, 5, 64, 16};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *map = it->second;
+      return 0;
+    }
+  }
+  static PFN_encodeTiled enc = nullptr;
+  if (!enc) {
+    enc = reinterpret_cast<PFN_encodeTiled>(driver_symbol("cuTensorMapEncodeTiled"));
+    if (!enc) return set_error("cuTensorMapEncodeTiled unavailable");
+  }
+  cuuint64_t dims[5] = {64, 16, 2, 2, (cuuint64_t)num_blocks * 2 * hkv};
+  cuuint64_t strides[4] = {256, 128, (cuuint64_t)hkv * 4096, 4096};
+  cuuint32_t box[5] = {64, 16, 2, 2, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(cache_layer), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_cu_error("cuTensorMapEncodeTiled(kv5d)", r);
+  std::lock_guard<std::mutex> lk(mu);
+  cache.emplace(key, *map);
+  return 0;
+}
+}  // namespace rb
+
+namespace rb {
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel): the attribute is
+// per device, so a process that launches on several GPUs sets it on each.
+cudaError_t set_smem_attr_once(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({dev, fn})) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert({dev, fn});
+  return e;
+}
 }  // namespace rb

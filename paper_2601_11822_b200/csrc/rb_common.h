@@ -20,6 +20,8 @@ void* driver_symbol(const char* name);
 // Encode a 2D bf16 tensor map: inner dim `inner` elements (contiguous), outer
 // dim `outer` rows with row stride `ld` elements; box = box_inner x box_outer,
 // 128-byte swizzle. Returns 0 or an error code.
+cudaError_t set_smem_attr_once(const void* fn, int bytes);
+int make_tmap_kv5d_bf16(CUtensorMap* map, const void* cache_layer, uint64_t num_blocks, int hkv);
 int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
                       uint32_t box_inner, uint32_t box_outer);
 

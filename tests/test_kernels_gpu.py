@@ -184,6 +184,63 @@ def test_decode_attention(Hq, Hkv, sms):
         assert rel_l2(out[b : b + 1], ref) < 1e-2, (b, n)
 
 
+@pytest.mark.parametrize("one_op", [0, 1])
+@pytest.mark.parametrize("shape", [1, 2, 3, 4])
+def test_decode_attention_load_modes(one_op, shape):
+    """Every ring shape (warps x stages) with both page-load forms: one 5D TMA op per page
+    (default) and four 2D {64, 16} boxes."""
+    lib = ops.load()
+    gen = torch.Generator(device=DEV).manual_seed(7 * shape + one_op)
+    D, nb, B, Hq, Hkv = 128, 512, 5, 32, 8
+    cache = _make_cache(nb, Hkv, D, gen)
+    seq = torch.tensor([3, 16, 33, 700, 1001], dtype=torch.int32, device=DEV)
+    maxb = 64
+    bt = torch.randperm(nb, device=DEV, generator=gen).int()[: B * maxb].view(B, maxb).contiguous()
+    slots = torch.arange(B, dtype=torch.int32, device=DEV)
+    q = torch.randn(B, Hq, D, device=DEV, generator=gen).bfloat16()
+    out = torch.zeros(B, Hq, D, device=DEV, dtype=torch.bfloat16)
+    ws = torch.zeros(B * Hq * 8 * (D + 2), device=DEV, dtype=torch.float32)
+    assert lib.rb_debug_decode_kv_one_op(one_op) == 0 and lib.rb_debug_decode_attn_shape(shape) == 0
+    try:
+        ops.decode_attention(q, cache, bt, slots, seq, out, num_kv_heads=Hkv, max_pages=maxb, workspace=ws,
+                             num_sms=40)
+        torch.cuda.synchronize()
+    finally:
+        lib.rb_debug_decode_kv_one_op(1)
+        lib.rb_debug_decode_attn_shape(0)
+    for b in range(B):
+        k, v = _gather_kv(cache, bt[b], int(seq[b]))
+        assert rel_l2(out[b : b + 1], _ref_attn(q[b : b + 1], k, v)) < 1e-2, b
+
+
+@pytest.mark.parametrize("sms", [148, 40])
+def test_decode_attention_growing_max(sms):
+    """Scores that grow along the context (and some that barely move) exercise the lazy
+    running max: pages that raise it by more than 2^8 in some heads but not others."""
+    gen = torch.Generator(device=DEV).manual_seed(5 + sms)
+    D, nb, B, Hq, Hkv = 128, 512, 4, 32, 8
+    cache = _make_cache(nb, Hkv, D, gen)
+    seq = torch.tensor([40, 333, 700, 1001], dtype=torch.int32, device=DEV)
+    maxb = 64
+    bt = torch.randperm(nb, device=DEV, generator=gen).int()[: B * maxb].view(B, maxb).contiguous()
+    ramp = torch.linspace(0.1, 8.0, 16 * maxb, device=DEV).view(maxb, 1, 16, 1)
+    for b in range(B):
+        pages = bt[b].long()
+        cache[pages, 0] = (cache[pages, 0].float() * ramp).bfloat16()
+    slots = torch.arange(B, dtype=torch.int32, device=DEV)
+    q = torch.randn(B, Hq, D, device=DEV, generator=gen)
+    q[:, ::3] *= 0.02  # some heads barely move their max
+    q = q.bfloat16()
+    out = torch.zeros(B, Hq, D, device=DEV, dtype=torch.bfloat16)
+    ws = torch.zeros(B * Hq * 16 * (D + 2), device=DEV, dtype=torch.float32)
+    ops.decode_attention(q, cache, bt, slots, seq, out, num_kv_heads=Hkv, max_pages=maxb, workspace=ws, num_sms=sms)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out).all()
+    for b in range(B):
+        k, v = _gather_kv(cache, bt[b], int(seq[b]))
+        assert rel_l2(out[b : b + 1], _ref_attn(q[b : b + 1], k, v)) < 1e-2, b
+
+
 def test_decode_attention_stale_nan_tail():
     """Rows past the sequence end in the last page may hold non-finite stale data."""
     gen = torch.Generator(device=DEV).manual_seed(21)
