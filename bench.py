@@ -118,7 +118,9 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def dist_setup():
+def dist_setup(backend: str = "nccl"):
+    """One process per GPU. backend "gloo" (TP peer modes) also allows several ranks on one
+    GPU: ranks map onto the visible devices round-robin."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -126,8 +128,13 @@ def dist_setup():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            local = local % max(1, torch.cuda.device_count())
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
     return rank, world, local
 
 
@@ -206,8 +213,9 @@ def _free_cuda():
     torch.cuda.empty_cache()
 
 
-def serve(args, arch, items, horizon, engine_kind, rank, world, local, *, primary):
-    """Serve `items` with one engine on this rank's GPU; returns the measurements."""
+def serve(args, arch, items, horizon, engine_kind, rank, world, local, *, primary, executor=None):
+    """Serve `items` with one engine on this rank's GPU; returns the measurements.
+    `executor`: a prebuilt executor (rank 0 of a TP group: tp_serve.build_tp_executor)."""
     import torch
 
     from paper_2601_11822_b200.arm import CostParams
@@ -229,8 +237,11 @@ def serve(args, arch, items, horizon, engine_kind, rank, world, local, *, primar
         hchunk = int(engine_kind.split("-", 1)[1])
         ex = HybridB200Executor(arch, seed=rank, max_batch=mb, chunk_tokens=hchunk, max_context=max_ctx,
                                 num_slots=4096)
+    elif executor is not None:
+        ex = executor
     else:
         ex = B200Executor(arch, seed=rank, static_decode_sms=None if args.arm else args.decode_sms, max_batch=mb,
+                          kv_memory_fraction=args.kv_memory_fraction,
                           chunk_tokens=2048, max_context=max_ctx, num_slots=4096, probe_attention=True)
     policy = None
     if args.arm_profile and not hybrid:
@@ -280,8 +291,7 @@ def serve(args, arch, items, horizon, engine_kind, rank, world, local, *, primar
             st["start_handle"] = h
             st["host0"] = time.perf_counter()
             st["h2d0"], st["d2h0"], st["launch0"] = ex.h2d_bytes, ex.d2h_bytes, ex.gpu_launches
-            if primary:
-                clocks.start()
+            clocks.start()  # both arms: the comparator's clocks are reported too
         if st["start_handle"] is not None and st["end_handle"] is None:
             st["steps"] += 1
             st["Bs"].append(len(members))
@@ -301,8 +311,7 @@ def serve(args, arch, items, horizon, engine_kind, rank, world, local, *, primar
             if h is win["end_handle"]:
                 win["host1"] = time.perf_counter()
                 win["h2d1"], win["d2h1"], win["launch1"] = ex.h2d_bytes, ex.d2h_bytes, ex.gpu_launches
-                if primary:
-                    win["clocks"] = clocks.stop()
+                win["clocks"] = clocks.stop()
 
     setattr(ex, launch_name, launch_decode)
     setattr(ex, finish_name, finish_decode)
@@ -310,7 +319,7 @@ def serve(args, arch, items, horizon, engine_kind, rank, world, local, *, primar
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    loop = RealTimeLoop(until_us=horizon)
+    loop = RealTimeLoop(until_us=horizon, poll_sleep_us=args.poll_sleep_us)
     loop_ref["loop"] = loop
     engine.prime(loop, items)
     t_run = time.perf_counter()
@@ -318,7 +327,7 @@ def serve(args, arch, items, horizon, engine_kind, rank, world, local, *, primar
     t_run = time.perf_counter() - t_run
     torch.cuda.synchronize()
     check_invariants(engine)
-    if primary and win.get("clocks") is None and clocks.proc is not None:
+    if win.get("clocks") is None and clocks.proc is not None:
         win["clocks"] = clocks.stop()
 
     complete = win["end_handle"] is not None and win["host1"] is not None
@@ -363,6 +372,7 @@ def serve(args, arch, items, horizon, engine_kind, rank, world, local, *, primar
         "probe": {"bytes": pb, "ms": pm, "launches": len(probe),
                   "by_sms": {str(k): {"gbs": v[0] / v[1] / 1e6 if v[1] else None, "launches": v[2]}
                              for k, v in sorted(by_part.items())}},
+        "host_gap": _gap_stats(getattr(ex, "host_gap_log", [])),
         "duty": {"decode": duty([(g, ns) for _, g, ns in ex.step_log], w0, w1),
                  "prefill": duty(getattr(ex, "prefill_log", []), w0, w1)},
         "run_wall_s": t_run, "requests": len(engine.requests),
@@ -383,6 +393,15 @@ def serve(args, arch, items, horizon, engine_kind, rank, world, local, *, primar
         ex.close()
     del engine
     return res
+
+
+def _gap_stats(log):
+    """Host time per decode step: from a step's completion handling to the next launch."""
+    if not log:
+        return None
+    xs = sorted(log)
+    return {"median_us": xs[len(xs) // 2], "mean_us": round(sum(xs) / len(xs), 1),
+            "p99_us": xs[min(len(xs) - 1, int(0.99 * len(xs)))], "steps": len(xs)}
 
 
 def _write_timeline(path, engine, ex, horizon_us):
@@ -427,6 +446,13 @@ def main():
     ap.add_argument("--compare", default="auto",
                     help="second arm on the same trace in the same run: hybrid-<chunk> | none (auto: hybrid-2048 "
                          "when --engine rapid)")
+    ap.add_argument("--poll-sleep-us", type=int, default=0,
+                    help="real-time loop sleep between CUDA-event polls (0 = busy-poll while GPU work is pending)")
+    ap.add_argument("--tp", type=int, default=1, help="cfg 4: tensor parallel over the whole job (world == tp)")
+    ap.add_argument("--tp-ar", default="nccl", choices=["nccl", "peer", "push"],
+                    help="TP all-reduce: NCCL (NVLink) or the peer-memory kernels (also several ranks on one GPU)")
+    ap.add_argument("--kv-memory-fraction", type=float, default=0.90,
+                    help="share of free HBM the KV cache takes (the reference's 10%% rule: 0.9)")
     ap.add_argument("--max-batch", type=int, default=256, help="engine max_batch of the primary arm (config.py:263)")
     ap.add_argument("--compare-max-batch", type=int, default=256, help="max_batch of the hybrid comparator")
     ap.add_argument("--slo-ms", type=float, default=SLO_ITL_US / 1e3, help="p99 ITL SLO (default 50 ms)")
@@ -459,10 +485,16 @@ def main():
     if args.decode_sms is None:
         args.decode_sms = 72
 
-    rank, world, local = dist_setup()
+    if args.tp > 1:  # cfg 4: one engine, tensor parallel over the whole job (no replicas, no comparator)
+        args.compare = "none"
+        args.arm = False
+        args.arm_profile = None
+    rank, world, local = dist_setup("gloo" if args.tp > 1 and args.tp_ar != "nccl" else "nccl")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if args.tp > 1 and world != args.tp:
+        raise SystemExit(f"--tp {args.tp} needs a world of {args.tp} ranks (got {world})")
 
     import torch
 
@@ -477,11 +509,43 @@ def main():
     # the run-level rate is not dominated by the ramp
     duration = args.duration or max(60.0, 8.0 + (args.warmup + args.steps) * 0.02 * 1.6)
     horizon = int(duration * 1e6)
-    items = shard_items(synthesize(WorkloadSpec(qps=args.qps * world, duration_s=duration, seed=42,
-                                                mean_prompt_tokens=PROMPT, mean_output_tokens=OUTPUT, sigma=0.0)),
-                        rank, world)
+    tp = args.tp if args.tp > 1 else 1
+    trace = synthesize(WorkloadSpec(qps=args.qps * (world // tp), duration_s=duration, seed=42,
+                                    mean_prompt_tokens=PROMPT, mean_output_tokens=OUTPUT, sigma=0.0))
+    channel = None
+    tp_ex = None
+    if tp > 1:
+        import torch.distributed as dist
 
-    main_res = serve(args, arch, items, horizon, args.engine, rank, world, local, primary=True)
+        from paper_2601_11822_b200.tp_engine import CommandChannel, attach_leader, serve_worker
+        from paper_2601_11822_b200.tp_serve import build_tp_executor
+
+        host = dist.new_group(backend="gloo")
+        tp_ex = build_tp_executor(arch, rank, world, host, ar=args.tp_ar, device=f"cuda:{local}",
+                                  static_decode_sms=args.decode_sms, max_batch=args.max_batch, chunk_tokens=2048,
+                                  max_context=PROMPT + OUTPUT + 64, num_slots=4096,
+                                  kv_memory_fraction=args.kv_memory_fraction, probe_attention=(rank == 0))
+        channel = CommandChannel(host)
+        if rank != 0:
+            tp_ex.warmup()  # the same captures, in the same order, as rank 0's serve()
+            n = serve_worker(tp_ex, channel)
+            print(json.dumps({"tp_rank": rank, "commands": n, "frames": channel.frames}), file=sys.stderr)
+            tp_ex.close()
+            return
+        attach_leader(tp_ex, channel)
+        items = trace
+    else:
+        items = shard_items(trace, rank, world)
+
+    if tp > 1:
+        try:
+            main_res = serve(args, tp_ex.arch, items, horizon, args.engine, 0, 1, local, primary=True, executor=tp_ex)
+        finally:
+            from paper_2601_11822_b200.tp_engine import stop_workers
+
+            stop_workers(channel)
+    else:
+        main_res = serve(args, arch, items, horizon, args.engine, rank, world, local, primary=True)
     ex = main_res.pop("ex", None)
     part = main_res.pop("part", None)
 
@@ -550,11 +614,13 @@ def main():
                          + f" at every launch; OVERALLOCATE -> both phases on {m['total_sms']} SMs, PARTITION -> "
                            f"green-context split)" if args.arm and args.engine == "rapid" else
                          f"{args.engine}: {args.model} bf16" if args.engine != "rapid" else
-                         f"cfg2: {args.model} bf16, static split decode {args.decode_sms} SMs")
+                         (f"cfg4: {args.model} bf16 TP={world} (rank 0 engine, workers replay its device "
+                          f"commands), static split decode {args.decode_sms} SMs" if args.tp > 1 else
+                          f"cfg2: {args.model} bf16, static split decode {args.decode_sms} SMs"))
                         + f", trace in {PROMPT}/out {OUTPUT} sigma=0 at {args.qps} QPS per replica for "
                           f"{duration:.0f} s, request i -> replica i mod {world}",
             "qps_per_replica": args.qps,
-            "parallelism": f"replicas x{world}",
+            "parallelism": f"tp{world} ({args.tp_ar} all-reduce)" if args.tp > 1 else f"replicas x{world}",
             "l2": "inputs > L2 (KV + weights ~30 GB per step); no flush",
             "step": "one decode iteration (CUDA-graph replay); prefill runs concurrently on its partition"
                     if args.engine == "rapid" else "one fused hybrid iteration (decode rows + one prefill chunk)",
@@ -598,6 +664,7 @@ def main():
         "run_wall_s": m["run_wall_s"],
         "arm_decisions": m["arm_decisions"],
         "stream_duty": m["duty"],
+        "host_loop": {"decode_completion_to_next_launch": m["host_gap"], "poll_sleep_us": args.poll_sleep_us},
         "requests": m["requests"],
         "finished": m["finished_all"],
         "profiles": os.path.join(ROOT, "profiles"),
@@ -611,6 +678,7 @@ def main():
             "device_window_tokens_per_s": comp["tokens"] / (comp["ms"] / 1e3) if comp["complete"] else None,
             "mean_decode_batch": comp["mean_batch"], "run_wall_s": comp["run_wall_s"],
             "max_batch": args.compare_max_batch,
+            "clocks": comp["clocks"],
             "note": "same trace, same engine code, same run; chunked-prefill hybrid batching on the whole device"}
         cv = constrained(cp)
         line["vs_comparator"] = value / cv if cv else None

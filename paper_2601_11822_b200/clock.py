@@ -206,3 +206,5 @@ class RealTimeLoop:
                         self.idle_us += wait - 100
                 elif self.poll_sleep_us > 0:
                     time.sleep(self.poll_sleep_us / 1e6)
+                # poll_sleep_us == 0: busy-poll the CUDA events (a completion is acted on within
+                # one cudaEventQuery sweep instead of a >= 50 us sleep granule)

@@ -94,8 +94,10 @@ __device__ __forceinline__ void tmem_ld_x32(uint32_t taddr, float (&v)[32]) {
 // causal pair g, nqb-1-g): every K/V tile is loaded once for both, and two warpgroups run
 // softmax while the tensor cores work on the other tile. The short tile of a pair needs
 // fewer key tiles (causal); its MMAs simply stop there.
+constexpr int pattn_threads(int tiles) { return 32 * (1 + tiles) + 128 * tiles; }
+
 template <int kTiles>
-__global__ void __launch_bounds__(64 + 128 * kTiles, 1)
+__global__ void __launch_bounds__(pattn_threads(kTiles), 1)
     prefill_attn_tc_kernel(const __grid_constant__ CUtensorMap q_map, const __grid_constant__ CUtensorMap kv_map,
                            const int* __restrict__ bt, int T, int start, int Hq, int Hkv,
                            __nv_bfloat16* __restrict__ out, long long out_tok_stride, float scale_log2) {
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(64 + 128 * kTiles, 1)
     mbar_init(q_full, 1);
     for (int st = 0; st < kStages; ++st) {
       mbar_init(&kv_full[st], 1);
-      mbar_init(&kv_empty[st], 1);
+      mbar_init(&kv_empty[st], kTiles);  // one commit / arrive per tile's MMA issuer
     }
     for (int i = 0; i < 2 * kTiles; ++i) {
       mbar_init(&s_full[i], 1);
@@ -208,63 +210,65 @@ __global__ void __launch_bounds__(64 + 128 * kTiles, 1)
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp <= kTiles) {
     if (lane == 0) {
-      // ================= MMA issuer =================
+      // ================= MMA issuers: warp 1 + w drives query tile w =================
+      // One issuer per tile decouples the tiles' S -> softmax -> P -> PV chains: S_{j+1}(w)
+      // is issued as soon as tile w's PV_{j-1} is, not after the other tile's softmax too
+      // (with one issuer the softmax warps waited on S ~40% of their time: profiles/r02/pattn/).
+      const int w = warp - 1;
+      const int nt = ntile[w];
       const uint32_t idesc_s = make_idesc_bf16(kBMq, kBN);
       const uint32_t idesc_o = make_idesc_bf16(kBMq, kD) | (1u << 16);  // B (V) MN-major
       mbar_wait(q_full, 0);
       tc_fence_after();
+      const uint32_t qa = smem_u32(sQ + w * kQBytes);
       auto issue_s = [&](int j) {
         const int st = j % kStages;
-        const uint32_t ph = (uint32_t)((j / kStages) & 1);
         const int b = j & 1;
-        mbar_wait(&kv_full[st], ph);
+        mbar_wait(&kv_full[st], (uint32_t)((j / kStages) & 1));
+        mbar_wait(&s_free[2 * w + b], (uint32_t)(((j >> 1) & 1) ^ 1));
+        tc_fence_after();
         const uint32_t kb = smem_u32(sKV + (size_t)st * kKVStage);
 #pragma unroll
-        for (int w = 0; w < kTiles; ++w) {
-          if (j >= ntile[w]) continue;
-          mbar_wait(&s_free[2 * w + b], (uint32_t)(((j >> 1) & 1) ^ 1));
-          tc_fence_after();
-          const uint32_t qa = smem_u32(sQ + w * kQBytes);
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint32_t off = (uint32_t)((kk & 3) * 32);
-            const uint64_t ad = sdesc_kmajor(qa + (kk >> 2) * (kQBytes / 2) + off);
-            const uint64_t bd = sdesc_kmajor(kb + (kk >> 2) * kKVHalf + off);
-            umma_bf16(tmem + s_col(w, b), ad, bd, idesc_s, kk > 0 ? 1u : 0u);
-          }
-          umma_commit(&s_full[2 * w + b]);
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (uint32_t)((kk & 3) * 32);
+          const uint64_t ad = sdesc_kmajor(qa + (kk >> 2) * (kQBytes / 2) + off);
+          const uint64_t bd = sdesc_kmajor(kb + (kk >> 2) * kKVHalf + off);
+          umma_bf16(tmem + s_col(w, b), ad, bd, idesc_s, kk > 0 ? 1u : 0u);
         }
+        umma_commit(&s_full[2 * w + b]);
       };
-      if (n_max > 0) issue_s(0);
-      for (int j = 0; j < n_max; ++j) {
-        if (j + 1 < n_max) issue_s(j + 1);
+      if (nt > 0) issue_s(0);
+      for (int j = 0; j < nt; ++j) {
+        if (j + 1 < nt) issue_s(j + 1);
         const int st = j % kStages;
         const int b = j & 1;
-        const uint32_t ph2 = (uint32_t)((j >> 1) & 1);
         const uint32_t vb = smem_u32(sKV + (size_t)st * kKVStage + 2 * kKVHalf);
+        mbar_wait(&p_full[2 * w + b], (uint32_t)((j >> 1) & 1));  // also orders any O rescale
+        tc_fence_after();
+        const uint32_t pa = smem_u32(sP + (size_t)(2 * w + b) * kPBytes);
 #pragma unroll
-        for (int w = 0; w < kTiles; ++w) {
-          if (j >= ntile[w]) continue;
-          mbar_wait(&p_full[2 * w + b], ph2);  // also orders any O rescale the softmax warps did
-          tc_fence_after();
-          const uint32_t pa = smem_u32(sP + (size_t)(2 * w + b) * kPBytes);
-#pragma unroll
-          for (int kk = 0; kk < kBN / 16; ++kk) {
-            const uint64_t ad = sdesc_kmajor(pa + kk * 32);
-            const uint64_t bd = sdesc_mnmajor(vb + kk * 2048, kKVHalf);
-            umma_bf16(tmem + o_col(w), ad, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
-          }
-          umma_commit(&o_full[2 * w + b]);
-          umma_commit(&p_free[2 * w + b]);
+        for (int kk = 0; kk < kBN / 16; ++kk) {
+          const uint64_t ad = sdesc_kmajor(pa + kk * 32);
+          const uint64_t bd = sdesc_mnmajor(vb + kk * 2048, kKVHalf);
+          umma_bf16(tmem + o_col(w), ad, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
         }
+        umma_commit(&o_full[2 * w + b]);
+        umma_commit(&p_free[2 * w + b]);
         umma_commit(&kv_empty[st]);
+      }
+      // key tiles past this query tile's diagonal (the short tile of a mirrored pair): release
+      // each stage once it has landed, so the producer's refill needs only the long tile
+      for (int j = nt; j < n_max; ++j) {
+        const int st = j % kStages;
+        mbar_wait(&kv_full[st], (uint32_t)((j / kStages) & 1));
+        mbar_arrive(&kv_empty[st]);
       }
     }
   } else {
     // ================= softmax warpgroups: thread = query row of tile w =================
-    const int w = (warp - 2) >> 2;
+    const int w = (warp - 1 - kTiles) >> 2;
     const int qd = warp & 3;
     const int row = qd * 32 + lane;
     const int q0 = qtile[w] * kBMq;
@@ -469,7 +473,7 @@ int prefill_attention_tc_launch(const void* q, long long q_tok_stride, const voi
   }
   if (smem > 227 * 1024) return set_error("prefill attn tc: shared memory budget exceeded");
   dim3 grid((nqb + tiles - 1) / tiles, Hq);
-  cudaError_t e = launch_k(fns[tiles - 1], dim3(grid), dim3(64 + 128 * tiles), smem, st, 1, qmap, kvmap, bt, T, start,
+  cudaError_t e = launch_k(fns[tiles - 1], dim3(grid), dim3(tiles == 2 ? pattn_threads(2) : pattn_threads(1)), smem, st, 1, qmap, kvmap, bt, T, start,
                            Hq, Hkv, reinterpret_cast<__nv_bfloat16*>(out), out_tok_stride, scale * 1.4426950408889634f);
   if (e != cudaSuccess) return set_cuda_error("prefill attn tc launch", e);
   return 0;

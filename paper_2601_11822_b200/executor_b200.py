@@ -79,7 +79,7 @@ class B200Executor:
                  num_blocks: int | None = None, kv_memory_fraction: float = 0.90, max_context: int | None = None,
                  num_slots: int = 1024, device: str = "cuda", token_source=None, use_graphs: bool = True,
                  batch_grid: tuple[int, ...] = DEFAULT_BATCH_GRID, serialize_phases: bool = False,
-                 record_logits: bool = False, probe_attention: bool = False):
+                 record_logits: bool = False, probe_attention: bool = False, vocab_offset: int = 0):
         self.arch = arch
         dev = torch.device(device)
         self.device = dev if dev.index is not None else torch.device("cuda", torch.cuda.current_device())
@@ -110,7 +110,8 @@ class B200Executor:
             raise RuntimeError("no HBM left for the KV cache")
         self.num_blocks = num_blocks
         self.runner = Runner(self.weights, num_blocks, num_slots, self.max_blocks_per_seq,
-                             max_prefill_tokens=max(chunk_tokens, 16), max_decode_batch=max_batch, device=self.device)
+                             max_prefill_tokens=max(chunk_tokens, 16), max_decode_batch=max_batch, device=self.device,
+                             vocab_offset=vocab_offset)
         # host mirrors / staging (pinned)
         self._slot_of: dict[int, int] = {}
         self._free_slots = list(range(num_slots - 1, -1, -1))
@@ -120,6 +121,7 @@ class B200Executor:
         self._upd_dev = {k: torch.zeros(1 + 3 * MAX_UPDATES, dtype=torch.int32, device=self.device)
                          for k in self._upd}
         self._dec_in_host = torch.zeros(3, max_batch, dtype=torch.int32, pin_memory=True)
+        self._dec_in_host_np = self._dec_in_host.numpy()
         self._dec_in_dev = torch.zeros(3, max_batch, dtype=torch.int32, device=self.device)
         d = self.runner.dec
         d.slot = self._dec_in_dev[0]
@@ -149,6 +151,8 @@ class B200Executor:
         self.gpu_launches = 0
         self.lazy_captures = 0
         self.step_log: list[tuple[int, int, int]] = []  # (B, gpu_us, host launch ns)
+        self.host_gap_log: list[int] = []  # us from a decode completion's handling to the next launch
+        self._t_fin_ns = None
         self.prefill_log: list[tuple[int, int]] = []  # (gpu_us, host launch ns)
         # in-situ decode-attention roofline: (algorithmic K+V bytes, kernel ms, decode SMs, host
         # launch ns) of the probed layer in every decode step (CUDA events inside the graphs)
@@ -291,7 +295,10 @@ class B200Executor:
             st = part.ds
             self._upd["decode"].extend(upd)
             self._flush_updates("decode", st)
-            self._dec_in_host[:, :bucket].copy_(torch.tensor([slots, pos, seq], dtype=torch.int32))
+            h = self._dec_in_host_np  # numpy view of the pinned staging rows (list -> int32 without torch)
+            h[0, :bucket] = slots
+            h[1, :bucket] = pos
+            h[2, :bucket] = seq
             with torch.cuda.stream(st):
                 self._dec_in_dev[:, :bucket].copy_(self._dec_in_host[:, :bucket], non_blocking=True)
                 if self.use_graphs:
@@ -391,14 +398,11 @@ class B200Executor:
         B = len(members)
         bucket = self._bucket(B)
         h = GpuHandle("decode", part.ds, part.d_sms / self.total_sms)
-        slots, pos, seq = [], [], []
-        lame = []
-        for r in members:
-            ctx = r.context_tokens
-            slots.append(self._slot_of[r.id])
-            pos.append(ctx - 1)
-            seq.append(ctx)
-            lame.append(r.delivered_tokens >= r.output_tokens)
+        slot_of = self._slot_of
+        seq = [r.prompt_tokens + len(r.token_times_us) for r in members]  # context_tokens (core.py:98-101)
+        slots = [slot_of[r.id] for r in members]
+        pos = [c - 1 for c in seq]
+        lame = [len(r.token_times_us) >= r.output_tokens for r in members]
         pad = bucket - B
         if pad:
             slots += [self.runner.dummy_slot] * pad
@@ -406,6 +410,9 @@ class B200Executor:
             seq += [0] * pad
         self._issue(("decode", self._partition_key(part), self._take_updates("decode"), B, bucket, slots, pos, seq))
         h.finish_record(part.ds)
+        if self._t_fin_ns is not None:  # host time from the previous step's completion to this launch
+            self.host_gap_log.append((time.perf_counter_ns() - self._t_fin_ns) // 1000)
+            self._t_fin_ns = None
         h.members = tuple(members)
         h.lame = lame
         h.d_sms = part.d_sms
@@ -417,6 +424,7 @@ class B200Executor:
     def finish_decode(self, handle) -> None:
         if handle is None:
             return
+        self._t_fin_ns = time.perf_counter_ns()
         out = self._dec_out_host[: len(handle.members)].tolist()
         rows = self.runner.dec.logits[: len(handle.members)].float().cpu() if self.record_logits else None
         for i, (r, is_lame, tok) in enumerate(zip(handle.members, handle.lame, out)):

@@ -7,6 +7,7 @@ import pytest
 
 from paper_2601_11822_b200.tp_engine import (CommandChannel, attach_leader, decode_command, encode_command,
                                              serve_worker, stop_workers)
+from paper_2601_11822_b200.tp_serve import agreed_num_blocks
 
 
 class _RecordingExecutor:
@@ -45,16 +46,17 @@ def _rank(rank, world, port, q, capacity):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     ch = CommandChannel(capacity=capacity)
+    agreed = agreed_num_blocks(1000 - 7 * rank, None)  # every rank's cache must hold rank 0's page ids
     ex = _RecordingExecutor()
     if rank == 0:
         attach_leader(ex, ch)
         for cmd in _commands():
             ex._issue(cmd)
         stop_workers(ch)
-        q.put((rank, ex.ran, ch.sent, ch.frames))
+        q.put((rank, ex.ran, ch.sent, ch.frames, agreed))
     else:
         n = serve_worker(ex, ch)
-        q.put((rank, ex.ran, n, ch.frames))
+        q.put((rank, ex.ran, n, ch.frames, agreed))
     dist.destroy_process_group()
 
 
@@ -83,7 +85,8 @@ def test_leader_commands_replay_on_worker(capacity):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    (_, leader_ran, sent, f0), (_, worker_ran, n, f1) = out
+    (_, leader_ran, sent, f0, a0), (_, worker_ran, n, f1, a1) = out
+    assert a0 == a1 == 993
     want = _commands()
     assert leader_ran == want
     assert worker_ran == want
