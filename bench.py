@@ -350,7 +350,7 @@ def serve(args, arch, items, horizon, engine_kind, rank, world, local, *, primar
         tk = torch.tensor([tokens, pb, pm], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(tk, op=torch.distributed.ReduceOp.SUM)
         ms, host_s, tokens, pb, pm = float(t[0]), float(t[1]), float(tk[0]), float(tk[1]), float(tk[2])
-    pooled = pool_window_stats(local_window_stats(engine.requests, slo, loop.horizon_us))
+    pooled = pool_window_stats(local_window_stats(engine.requests, slo, loop.horizon_us), pool=world > 1)
 
     steps = max(1, win["steps"])
 
@@ -495,6 +495,10 @@ def main():
         return
     if args.tp > 1 and world != args.tp:
         raise SystemExit(f"--tp {args.tp} needs a world of {args.tp} ranks (got {world})")
+    if os.environ.get("RB_WATCHDOG_S"):  # debug: every thread's Python stack to stderr, then exit
+        import faulthandler
+
+        faulthandler.dump_traceback_later(float(os.environ["RB_WATCHDOG_S"]), exit=True)
 
     import torch
 

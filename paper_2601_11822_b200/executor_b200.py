@@ -23,6 +23,8 @@ extensions on the decode stream before the step that needs them.
 from __future__ import annotations
 
 import math
+import os
+import sys
 import time
 
 import torch
@@ -386,9 +388,12 @@ class B200Executor:
             return
         keys = decode_sms_list if decode_sms_list is not None else (
             [self.static_decode_sms] if self.static_decode_sms is not None else [None])
+        dbg = os.environ.get("RB_DEBUG_WARMUP")
         for k in keys:
             part = self._partition(k) if k is not None else self._partitions[None]
             for b in self.grid:
+                if dbg:
+                    print(f"[warmup pid {os.getpid()}] partition {k} bucket {b}", file=sys.stderr, flush=True)
                 self._capture(part, b)
         torch.cuda.synchronize()
         self.lazy_captures = 0  # captures counted from here on happened while serving

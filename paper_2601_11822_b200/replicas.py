@@ -66,7 +66,7 @@ def local_window_stats(requests, slo, horizon_us: int) -> dict:
     }
 
 
-def pool_window_stats(local: dict, group=None) -> dict:
+def pool_window_stats(local: dict, group=None, pool: bool = True) -> dict:
     """Whole-job run-level metrics over all replicas: tokens/s = all in-window stamps / the
     (common) window, p99 ITL / p50 TTFT nearest-rank over the POOLED samples of every replica
     (not a max of per-rank percentiles). Every rank gets the result."""
@@ -75,7 +75,8 @@ def pool_window_stats(local: dict, group=None) -> dict:
     from paper_2601_11822_b200.slo import percentile_nearest_rank
 
     parts = [local]
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+    # pool=False: this rank's engine is the whole job (rank 0 of a TP group)
+    if pool and dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         parts = [None] * dist.get_world_size(group)
         dist.all_gather_object(parts, local, group=group)
     window = max(p["window_s"] for p in parts)

@@ -22,7 +22,12 @@ one 64 KB broadcast per launch, no pickling and no length round trip.
 
 from __future__ import annotations
 
+import os
+import sys
+
 import numpy as np
+
+_DEBUG = bool(os.environ.get("RB_DEBUG_TP"))
 
 STOP = ("stop",)
 CAPACITY = 16384  # int32 words per frame
@@ -101,6 +106,8 @@ class CommandChannel:
         self.frames += 1
 
     def send(self, cmd) -> None:
+        if _DEBUG:
+            print(f"[tp leader] send #{self.sent} {cmd[0]}", file=sys.stderr, flush=True)
         words = encode_command(cmd)
         f = self._frame.numpy()
         for off in range(0, words.shape[0], self.capacity):
@@ -140,5 +147,7 @@ def serve_worker(executor, channel: CommandChannel) -> int:
         cmd = channel.recv()
         if cmd == STOP:
             return n
+        if _DEBUG:
+            print(f"[tp worker] run #{n} {cmd[0]}", file=sys.stderr, flush=True)
         executor.run_command(cmd)
         n += 1

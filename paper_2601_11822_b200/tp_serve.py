@@ -40,9 +40,10 @@ def agreed_num_blocks(local_blocks: int, host_group) -> int:
 
 
 def build_tp_executor(arch: ArchConfig, rank: int, world: int, host_group, *, ar: str = "nccl",
-                      device: str = "cuda", **executor_kw) -> B200Executor:
+                      device: str = "cuda", state: dict | None = None, **executor_kw) -> B200Executor:
     """This rank's sharded executor with its collectives attached (see the module docstring).
 
+    `state`: a full-model fp32 state dict to shard (default: random weights of the real shapes).
     `ar`: "nccl" (mode 1; NVLink / NVSwitch across GPUs), "peer" (mode 2: one-shot pull
     all-reduce over cudaIpc-mapped peer buffers) or "push" (mode 3: the row-parallel GEMM's
     epilogue stores its tiles into every rank). Peer modes also run with several ranks on one
@@ -53,7 +54,12 @@ def build_tp_executor(arch: ArchConfig, rank: int, world: int, host_group, *, ar
         raise ValueError(f"tp: all-reduce mode {ar!r} (nccl | peer | push)")
     la = local_arch(arch, world)
     dev = torch.device(device)
-    weights = DecoderWeights.random(la, device=dev, seed=rank, embed_vocab=arch.vocab)
+    if state is not None:  # this rank's slice of a full fp32 state (parity tests: tp.shard_state)
+        from paper_2601_11822_b200.tp import shard_state
+
+        weights = DecoderWeights.from_state(la, shard_state(arch, state, rank, world), device=dev)
+    else:
+        weights = DecoderWeights.random(la, device=dev, seed=rank, embed_vocab=arch.vocab)
     ex = B200Executor(la, weights=weights, vocab_offset=rank * la.vocab,
                       token_source=lambda req: prompt_token_ids(req.id, req.prompt_tokens, arch.vocab),
                       **executor_kw)

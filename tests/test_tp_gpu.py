@@ -129,3 +129,74 @@ def test_nccl_world1_identity():
     assert int(base.dec.out_ids[0]) == int(tp.dec.out_ids[0])
     assert torch.equal(base.kv, tp.kv)
     comms.close()
+
+
+def _tp_serve_rank(rank, world, port, out_dir, ar):
+    import os
+
+    import torch.distributed as dist
+
+    from paper_2601_11822_b200.arm import CostParams
+    from paper_2601_11822_b200.engines.rapid import RapidEngine
+    from paper_2601_11822_b200.harness import run_items
+    from paper_2601_11822_b200.slo import SloSpec
+    from paper_2601_11822_b200.specs import b200_spec
+    from paper_2601_11822_b200.tp_engine import CommandChannel, attach_leader, serve_worker, stop_workers
+    from paper_2601_11822_b200.tp_serve import build_tp_executor
+    from paper_2601_11822_b200.traffic import WorkloadSpec, synthesize
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    arch = ARCHS["tiny"]
+    ex = build_tp_executor(arch, rank, world, None, ar=ar, state=init_state(arch, seed=0), static_decode_sms=72,
+                           max_batch=16, chunk_tokens=32, num_blocks=256, max_context=512, num_slots=32)
+    ch = CommandChannel()
+    ex.warmup()
+    if rank == 0:
+        attach_leader(ex, ch)
+        items = synthesize(WorkloadSpec(qps=16.0, duration_s=2.0, seed=0, mean_prompt_tokens=64,
+                                        mean_output_tokens=16))[:6]
+        model = arch.model_spec()
+        slo = SloSpec(itl_slo_us=50_000)
+        try:
+            res = run_items("rapid", items, model, b200_spec(), CostParams(), slo,
+                            engine_factory=lambda: RapidEngine(model, b200_spec(), CostParams(), slo, chunk_tokens=32,
+                                                               max_batch=16, executor=ex))
+        finally:
+            stop_workers(ch)
+        done = {r.id: (r.prompt_tokens, ex.generated[r.id]) for r in res.engine.requests
+                if r.state.value == "finished"}
+        torch.save({"done": done, "n": len(items)}, os.path.join(out_dir, "served.pt"))
+    else:
+        serve_worker(ex, ch)
+    ex.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ar", ["peer", "push"])
+def test_tp2_serving_exact_greedy(tmp_path, ar):
+    """cfg-4 serving path (tp_serve + tp_engine) at world 2 on one GPU: rank 0's RapidEngine
+    drives both shards through the int32 command channel; every finished request's greedy ids
+    equal the fp32 oracle's (teacher-forced), i.e. the sharded forward, the command replay and
+    the vocab-parallel argmax agree end to end."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    from paper_2601_11822_b200.traffic import prompt_token_ids
+
+    arch = ARCHS["tiny"]
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    mp.spawn(_tp_serve_rank, args=(2, port, str(tmp_path), ar), nprocs=2, join=True)
+    out = torch.load(tmp_path / "served.pt")
+    assert len(out["done"]) == out["n"]
+    orc = Oracle(arch, init_state(arch, seed=0))
+    for rid, (P, gen) in out["done"].items():
+        prompt = prompt_token_ids(rid, P, arch.vocab).long()
+        logits, _ = orc.forward(torch.cat([prompt, torch.tensor(gen[:-1], dtype=torch.long)]), 0, None)
+        want = [int(x) for x in logits[P - 1 :].argmax(-1)]
+        assert gen == want, (rid, gen, want)
