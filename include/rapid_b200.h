@@ -57,6 +57,9 @@ int rb_debug_decode_kv_one_op(int on);
 /* Debug: decode attention ring shape, 0 = auto (default), 1..4 = 12x2, 8x3, 6x4, 4x6
  * (warps per CTA x smem stages per warp). Returns -1 for an invalid shape. */
 int rb_debug_decode_attn_shape(int shape);
+/* Debug: decode (swap-AB) GEMMs as data-parallel K-slice units writing fp32 partials
+ * [s][token][feature] into the workspace (no output written; timing experiments), 0 = off. */
+int rb_debug_gemm_ksplit(int s);
 /* Debug (diagnostic, csrc/probe.cu): stream `bytes` of global memory into shared memory with
  * 1D bulk copies over a ring of `stages` x `chunk` bytes, one CTA per SM, no compute — the
  * per-SM ingest ceiling of a partition. `sink` is a device int the kernel may write. */
@@ -71,6 +74,9 @@ int rb_debug_stream_read_tma(const void* src, long long bytes, int box_rows, int
 int rb_set_pdl(int on);
 /* Decode (swap-AB) gate|up GEMM: 1 = SwiGLU fused into its epilogue, 0 = separate kernel. */
 int rb_set_decode_glu(int on);
+/* Decode-only single-GPU iterations: O / down projections as K-slice units whose fp32 partials
+ * the following RMSNorm adds to the residual stream (default 1); 0 = stream-K + residual epilogue. */
+int rb_set_decode_ksplit(int on);
 
 /* K1/K4 — bf16 linear layer on tcgen05 tensor cores:
  *   Y[t,o] = sum_k X[t,k] W[o,k] (+bias[o]) (+R[t,o])

@@ -32,6 +32,7 @@ int gemm_set_prefill_bn(int bn);
 int prefill_attn_set_tiles(int tiles);
 int decode_attn_set_kv_ops(int one_op);
 int decode_attn_set_shape(int shape);
+int gemm_set_ksplit(int s);
 int stream_read_launch(const void* src, long long bytes, int chunk, int stages, int num_sms, int* sink,
                        cudaStream_t st);
 int stream_read_tma_launch(const void* src, long long bytes, int box_rows, int per_stage, int stages, int num_sms,
@@ -53,6 +54,7 @@ int rb_debug_gemm_prefill_bn(int bn) { return rb::gemm_set_prefill_bn(bn); }
 int rb_debug_pattn_tiles(int tiles) { return rb::prefill_attn_set_tiles(tiles); }
 int rb_debug_decode_kv_one_op(int on) { return rb::decode_attn_set_kv_ops(on); }
 int rb_debug_decode_attn_shape(int shape) { return rb::decode_attn_set_shape(shape); }
+int rb_debug_gemm_ksplit(int s) { return rb::gemm_set_ksplit(s); }
 int rb_debug_stream_read(const void* src, long long bytes, int chunk, int stages, int num_sms, int* sink,
                          void* stream) {
   return rb::stream_read_launch(src, bytes, chunk, stages, num_sms, sink, static_cast<cudaStream_t>(stream));

@@ -70,6 +70,91 @@ int rmsnorm_launch(const void* x, long long ldx, const void* w, void* y, long lo
   return e == cudaSuccess ? 0 : set_cuda_error("rmsnorm launch", e);
 }
 
+// Consumer of a K-sliced decode GEMM (O / down projection, gemm mode bit 16): the residual
+// stream row x[t] += sum over slices s (in order) of the fp32 partial P[s][t][:], rounded to
+// bf16 and written back, then y[t] = rmsnorm(x[t]) * w — the split-K reduction rides on the
+// RMSNorm that follows anyway (no finisher SM in the GEMM). The sum of squares is taken over
+// the rounded row, as rmsnorm_kernel reads it.
+__global__ void add_partials_rmsnorm_kernel(const float* __restrict__ part, int ks, long long slice,
+                                            __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
+                                            __nv_bfloat16* __restrict__ y, int H, float eps) {
+  pdl_trigger();
+  pdl_wait();
+  extern __shared__ __align__(16) uint8_t rowbuf[];  // the updated row, bf16
+  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(rowbuf);
+  const int row = blockIdx.x;
+  __nv_bfloat16* xr = x + (size_t)row * H;
+  float ss = 0.f;
+  for (int i = threadIdx.x * 8; i < H; i += blockDim.x * 8) {
+    const uint4 u = *reinterpret_cast<const uint4*>(xr + i);
+    const uint32_t xv[4] = {u.x, u.y, u.z, u.w};
+    float a[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = unpack_bf16x2(xv[j]);
+      a[2 * j] = f.x;
+      a[2 * j + 1] = f.y;
+    }
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int sl = 0; sl < ks; ++sl) {
+      const float4* pp = reinterpret_cast<const float4*>(part + sl * slice + (size_t)row * H + i);
+      const float4 p0 = __ldcg(pp), p1 = __ldcg(pp + 1);
+      acc[0] += p0.x; acc[1] += p0.y; acc[2] += p0.z; acc[3] += p0.w;
+      acc[4] += p1.x; acc[5] += p1.y; acc[6] += p1.z; acc[7] += p1.w;
+    }
+    uint32_t ov[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      ov[j] = pack_bf16x2(a[2 * j] + acc[2 * j], a[2 * j + 1] + acc[2 * j + 1]);
+      const float2 r = unpack_bf16x2(ov[j]);
+      ss += r.x * r.x + r.y * r.y;
+    }
+    const uint4 o4 = make_uint4(ov[0], ov[1], ov[2], ov[3]);
+    *reinterpret_cast<uint4*>(xr + i) = o4;
+    *reinterpret_cast<uint4*>(xs + i) = o4;
+  }
+  __shared__ float red[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float inv = rsqrtf(red[0] / (float)H + eps);
+  __nv_bfloat16* yr = y + (size_t)row * H;
+  for (int i = threadIdx.x * 8; i < H; i += blockDim.x * 8) {
+    const uint4 u = *reinterpret_cast<const uint4*>(xs + i);
+    const uint4 wu = *reinterpret_cast<const uint4*>(w + i);
+    const uint32_t xv[4] = {u.x, u.y, u.z, u.w};
+    const uint32_t ww[4] = {wu.x, wu.y, wu.z, wu.w};
+    uint32_t ov[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = unpack_bf16x2(xv[j]);
+      const float2 g = unpack_bf16x2(ww[j]);
+      ov[j] = pack_bf16x2(f.x * inv * g.x, f.y * inv * g.y);
+    }
+    *reinterpret_cast<uint4*>(yr + i) = make_uint4(ov[0], ov[1], ov[2], ov[3]);
+  }
+}
+
+int add_partials_rmsnorm_launch(const float* part, int ks, long long slice, void* x, const void* w, void* y, int T,
+                                int H, float eps, cudaStream_t st) {
+  if (T <= 0) return 0;
+  if (H % 8 || ks < 1) return set_error("add_partials_rmsnorm: H % 8 == 0, ks >= 1");
+  int threads = H / 8;
+  if (threads > 1024) threads = 1024;
+  threads = ((threads + 31) / 32) * 32;
+  cudaError_t e = launch_k(add_partials_rmsnorm_kernel, dim3(T), dim3(threads), (size_t)H * 2, st, 1, part, ks, slice,
+                           (__nv_bfloat16*)x, (const __nv_bfloat16*)w, (__nv_bfloat16*)y, H, eps);
+  return e == cudaSuccess ? 0 : set_cuda_error("add_partials_rmsnorm launch", e);
+}
+
 // ------------------------------------------------------------------ RoPE + paged KV write
 // qkv row layout: [Hq*D | Hkv*D | Hkv*D]. Rotates q and k (neox / rotate_half
 // pairing i <-> i+D/2) at position pos[t], writes q to q_out and k, v into the

@@ -41,6 +41,11 @@ int tp_argmax(void* tp, const void* logits, long long ld, int T, int V_local, in
 }  // namespace rb
 
 // swap-AB (decode) gate|up: 1 = SwiGLU fused into the GEMM epilogue, 0 = separate kernel
+static int g_decode_ksplit = 1;  // decode O / down as K-slice partials summed in the following RMSNorm
+extern "C" int rb_set_decode_ksplit(int on) {
+  g_decode_ksplit = on ? 1 : 0;
+  return 0;
+}
 static int g_decode_glu = 0;
 extern "C" int rb_set_decode_glu(int on) {
   g_decode_glu = on;
@@ -92,9 +97,18 @@ extern "C" int rb_decoder_forward(const rb_model_t* m, const rb_workspace_t* w, 
       RB_TRY(embed_launch(w->ids, nullptr, nullptr, m->embed, x, nd, H, nullptr, st));
   }
   if (np > 0) RB_TRY(embed_launch(w->ids + nd, nullptr, nullptr, m->embed, x + (size_t)nd * H * e, np, H, nullptr, st));
+  // Decode-only iterations on a single GPU: the O and down projections run as K-slice units
+  // writing fp32 partials (gemm mode bits 8..11) and the RMSNorm that follows each adds them to
+  // the residual stream (add_partials_rmsnorm) — the split-K reduction without a finisher SM.
+  const bool ksplit_ok = g_decode_ksplit && np == 0 && tp == nullptr && w->gemm_ws != nullptr;
+  const int ks_o = ksplit_ok ? gemm_pick_ksplit(H, T, Hq * D, sms, w->gemm_ws_bytes) : 1;
+  const int ks_d = ksplit_ok ? gemm_pick_ksplit(H, T, I, sms, w->gemm_ws_bytes) : 1;
+  const float* part = static_cast<const float*>(w->gemm_ws);
+  bool h_ready = false;  // h already holds ln1(x) of this layer (fused into the previous down's consumer)
   for (int l = 0; l < m->layers; ++l) {
     char* cache = static_cast<char*>(m->kv_cache) + (size_t)l * m->kv_layer_stride_bytes;
-    RB_TRY(rmsnorm_launch(x, H, m->ln1[l], h, H, T, H, m->rms_eps, st));
+    if (!h_ready) RB_TRY(rmsnorm_launch(x, H, m->ln1[l], h, H, T, H, m->rms_eps, st));
+    h_ready = false;
     if (m->qk_layout == 1) {
       // q|k rows pair-interleaved: RoPE and the paged K/V write run in the QKV GEMM's
       // epilogue (no qkv round trip through HBM, no separate RoPE kernel)
@@ -121,17 +135,24 @@ extern "C" int rb_decoder_forward(const rb_model_t* m, const rb_workspace_t* w, 
                                          m->block_table + (size_t)b->prefill_slot * m->bt_stride, np,
                                          b->prefill_start, Hq, Hkv, D, attn + (size_t)nd * Hq * D * e,
                                          (long long)Hq * D, m->attn_scale, m->num_blocks, st));
-    {  // row-parallel under TP: partial -> all-reduce with the residual add
-      const void* res = x;
-      void* y = tp_gemm_out(tp, x, &res);
-      GemmPush push{};
-      const bool pushed = tp_gemm_push(tp, &push);  // mode 3: the epilogue stores into every rank
-      RB_TRY(gemm_bf16_launch(attn, m->wo[l], y, nullptr, res, T, H, Hq * D, Hq * D, Hq * D, H, 0, sms, w->gemm_ws,
-                              w->gemm_ws_bytes, w->gemm_counters, w->gemm_counters_len, st, nullptr,
-                              pushed ? &push : nullptr));
-      RB_TRY(tp_reduce(tp, x, (long long)T * H, st));
+    if (ks_o > 1) {
+      RB_TRY(gemm_bf16_launch(attn, m->wo[l], nullptr, nullptr, nullptr, T, H, Hq * D, Hq * D, Hq * D, H,
+                              2 | (ks_o << 8), sms, w->gemm_ws, w->gemm_ws_bytes, w->gemm_counters,
+                              w->gemm_counters_len, st));
+      RB_TRY(add_partials_rmsnorm_launch(part, ks_o, (long long)T * H, x, m->ln2[l], h, T, H, m->rms_eps, st));
+    } else {
+      {  // row-parallel under TP: partial -> all-reduce with the residual add
+        const void* res = x;
+        void* y = tp_gemm_out(tp, x, &res);
+        GemmPush push{};
+        const bool pushed = tp_gemm_push(tp, &push);  // mode 3: the epilogue stores into every rank
+        RB_TRY(gemm_bf16_launch(attn, m->wo[l], y, nullptr, res, T, H, Hq * D, Hq * D, Hq * D, H, 0, sms, w->gemm_ws,
+                                w->gemm_ws_bytes, w->gemm_counters, w->gemm_counters_len, st, nullptr,
+                                pushed ? &push : nullptr));
+        RB_TRY(tp_reduce(tp, x, (long long)T * H, st));
+      }
+      RB_TRY(rmsnorm_launch(x, H, m->ln2[l], h, H, T, H, m->rms_eps, st));
     }
-    RB_TRY(rmsnorm_launch(x, H, m->ln2[l], h, H, T, H, m->rms_eps, st));
     // gate|up (rows interleaved in 16-blocks): token-major tiles fuse the SwiGLU into the
     // GEMM epilogue; swap-AB (decode) tiles measured faster with the separate kernel.
     if (T > 256 || g_decode_glu) {
@@ -143,7 +164,15 @@ extern "C" int rb_decoder_forward(const rb_model_t* m, const rb_workspace_t* w, 
                               w->gemm_ws_bytes, w->gemm_counters, w->gemm_counters_len, st));
       RB_TRY(silu_mul_interleaved_launch(gu, 2 * I, act, I, T, I, st));
     }
-    {
+    if (ks_d > 1) {
+      RB_TRY(gemm_bf16_launch(act, m->wd[l], nullptr, nullptr, nullptr, T, H, I, I, I, H, 2 | (ks_d << 8), sms,
+                              w->gemm_ws, w->gemm_ws_bytes, w->gemm_counters, w->gemm_counters_len, st));
+      // the residual add rides on the next layer's ln1 (or, after the last layer, on the final
+      // norm, which the sampling rows below then skip)
+      const void* wn = l + 1 < m->layers ? m->ln1[l + 1] : m->final_norm;
+      RB_TRY(add_partials_rmsnorm_launch(part, ks_d, (long long)T * H, x, wn, h, T, H, m->rms_eps, st));
+      h_ready = true;
+    } else {
       const void* res = x;
       void* y = tp_gemm_out(tp, x, &res);
       GemmPush push{};
@@ -153,10 +182,11 @@ extern "C" int rb_decoder_forward(const rb_model_t* m, const rb_workspace_t* w, 
       RB_TRY(tp_reduce(tp, x, (long long)T * H, st));
     }
   }
+  const bool final_normed = h_ready;  // h = final_norm(x) for every (decode) row already
   // ---- sampling rows: decode rows, plus the chunk's last row when it finishes a prompt
   int nl = 0;
   if (b->logits_decode && nd > 0) {
-    RB_TRY(rmsnorm_launch(x, H, m->final_norm, h, H, nd, H, m->rms_eps, st));
+    if (!final_normed) RB_TRY(rmsnorm_launch(x, H, m->final_norm, h, H, nd, H, m->rms_eps, st));
     nl = nd;
   }
   if (b->emit_prefill && np > 0) {

@@ -76,6 +76,9 @@ struct GemmArgs {
   GemmRope rp;    // rp.q_out != nullptr: fused RoPE + paged K/V write epilogue (QKV projection)
   GemmPush push;  // push.world > 0: tiles go to every TP rank's receive slot (tp.cu mode 3)
   unsigned long long* trace;  // debug timeline: [cta][8] globaltimer stamps of this launch, or null
+  int ksplit;        // > 1 (decode): units = tiles x ksplit K-slices, each writes an fp32 partial slice
+  float* part;       // ksplit partials [ksplit][N_valid tokens][M_valid features] (swap orientation)
+  long long part_slice;  // floats per slice
 };
 
 // Work schedule shared by the producer, MMA and epilogue roles. Data-parallel: whole
@@ -95,12 +98,14 @@ __device__ __forceinline__ int sk_owner(const GemmArgs& g, int x, int ncl) {
 }
 struct SegIter {
   int lo, it;   // stream-K: this cluster's run [lo, it), walked from the END (descending)
-  int t, step;  // data-parallel cursor
+  int t, step;  // data-parallel cursor (units = tiles x ksplit)
+  int slice;    // K-slice of the current unit (ksplit > 1)
   __device__ __forceinline__ SegIter(const GemmArgs& g, int cid, int ncl) {
     lo = sk_start(g, cid, ncl);
     it = sk_start(g, cid + 1, ncl);
     t = cid;
     step = ncl;
+    slice = 0;
   }
   __device__ __forceinline__ bool next(const GemmArgs& g, int& tile, int& kb0, int& kb1) {
     if (g.streamk) {
@@ -113,10 +118,11 @@ struct SegIter {
       it = seg_lo;
       return true;
     }
-    if (t >= g.total_tiles) return false;
-    tile = t;
-    kb0 = 0;
-    kb1 = g.num_kb;
+    if (t >= g.total_tiles * g.ksplit) return false;
+    tile = t % g.total_tiles;
+    slice = t / g.total_tiles;
+    kb0 = (int)(((long long)slice * g.num_kb) / g.ksplit);
+    kb1 = (int)(((long long)(slice + 1) * g.num_kb) / g.ksplit);
     t += step;
     return true;
   }
@@ -638,7 +644,27 @@ __global__ void __launch_bounds__(threads_for(kSets), 1)
           else mbar_arrive(&tempty[acc]);
         }
       };
-      if (kb0 == 0 && kb1 == g.num_kb) {
+      if (kSets == 2 && g.ksplit > 1) {  // (decode kernels only: compiled out of the prefill ones)
+        // K-slice unit (decode): the fp32 partial of this slice goes to its own slot, row-major
+        // in the output orientation [token][feature]; the consumer kernel (RoPE / residual +
+        // RMSNorm) sums the slices in order — no finisher SM, no wait (deterministic)
+        float* slot = g.part + (size_t)seg.slice * g.part_slice;
+        for (int i = 0; i < MT; ++i) {
+          const int m0 = mbase + i * kBM * kPair;
+          const int f = m0 + lane;  // this lane's feature (MMA row)
+          for (int c = set; c < nchunk; c += kEpiSets) {
+            uint32_t v[32];
+            tmem_ld_sum(tbase + (uint32_t)(i * BN + c * 32), KA, sub_stride, v);
+            const int n0 = nt * BN + c * 32;
+            if (f < g.M_valid) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (n0 + j < g.N_valid) __stcg(slot + (size_t)(n0 + j) * g.M_valid + f, __uint_as_float(v[j]));
+            }
+          }
+        }
+        release_acc();
+      } else if (kb0 == 0 && kb1 == g.num_kb) {
         // whole tile in this segment: straight to Y
         for (int i = 0; i < MT; ++i) {
           const int m0 = mbase + i * kBM * kPair;
@@ -796,6 +822,43 @@ int gemm_set_prefill_bn(int bn) {
   g_prefill_bn = bn;
   return 0;
 }
+// Decode (swap-AB) K-slice count for a GEMM whose consumer sums fp32 partials (O / down ->
+// add_partials_rmsnorm): 1 = keep the stream-K schedule with the residual epilogue. Whole
+// K-slice units run with no finisher; used where two slices fit one wave of clusters (8B:
+// partitions >= 64 SMs), measured on 72 SMs: O 28.4 -> 19.7 us, down 49.3 -> 42.7 us (B=256),
+// whole decode step 8.91 -> 8.54 ms (B=128) / 13.18 -> 12.75 ms (B=256) alone
+// (profiles/r02/gemm/).
+int gemm_pick_ksplit(int O, int T, int K, int num_sms, size_t ws_bytes) {
+  if (T < 96 || T > 256 || K % kBK != 0 || num_sms < 2) return 1;  // MT = 1 swap-AB tiles only
+  const int BN = ((T + 31) / 32) * 32;
+  const int pair = (O > kBM && (BN > 128 || (BN == 128 && num_sms < 100))) ? 2 : 1;
+  const int clusters = num_sms / pair;
+  const int tiles = (O + kBM * pair - 1) / (kBM * pair);
+  const int nkb = K / kBK;
+  const double sk = (double)tiles * nkb / clusters;  // stream-K k-blocks per cluster
+  int best = 1;
+  double best_cost = 1e30;
+  // two slices at most: every slice is T x O fp32 the consumer re-reads (3 slices on 48 SMs won
+  // 10 us per layer in the GEMMs and lost it in the consumer: decode step unchanged)
+  for (int ks = 2; ks <= 2; ++ks) {
+    if (nkb < 2 * ks || (size_t)ks * T * O * sizeof(float) > ws_bytes) continue;
+    const double cost = (double)((tiles * ks + clusters - 1) / clusters) * ((nkb + ks - 1) / ks);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = ks;
+    }
+  }
+  // stream-K's even share pays a finisher (one SM sums 96 KB partials per contributor): K-slices
+  // win up to ~20% more k-blocks per unit (72 SMs, O: 32 vs 28.4 k-blocks, 19.7 vs 28.4 us)
+  return (best > 1 && best_cost <= 1.2 * sk + 4) ? best : 1;
+}
+
+static int g_ksplit = 0;  // debug (decode, swap-AB): > 1 = data-parallel K-slices with fp32 partial output
+int gemm_set_ksplit(int s) {
+  if (s < 0 || s > 16) return -1;
+  g_ksplit = s;
+  return 0;
+}
 static int g_prefill_streamk = 0;          // stream-K for badly wave-quantized token-major GEMMs
 static double g_prefill_streamk_frac = 0.6;
 int gemm_set_prefill_streamk(int on, double max_frac) {
@@ -829,7 +892,10 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
     return set_error("gemm: Y/residual/bias must be 16-byte aligned with ldy % 8 == 0");
   const int glu = (mode & 4) ? 1 : 0;      // flag bit: fused SwiGLU epilogue
   const int blocked = (mode & 8) ? 1 : 0;  // flag bit: W is block-packed (see rb_pack_weight)
+  const int ks_req = (mode >> 8) & 15;     // bits 8..11: decode K-slices with fp32 partial output (no Y)
   mode &= 3;
+  if (ks_req > 1 && (bias != nullptr || residual != nullptr || glu || rope != nullptr || push != nullptr))
+    return set_error("gemm: K-sliced partial output takes no bias / residual / SwiGLU / RoPE / push");
   if (glu && (O % 32 != 0 || bias != nullptr || residual != nullptr))
     return set_error("gemm: SwiGLU epilogue needs O % 32 == 0 and no bias / residual");
   if (mode == 0) mode = (T <= 256) ? 2 : 1;
@@ -932,6 +998,21 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
       g.streamk = 1;
       clusters = ncl;
     }
+  }
+  g.ksplit = 1;
+  const int ks_use = ks_req > 1 ? ks_req : g_ksplit;
+  if (ks_req > 1 && !(swap && MT == 1 && workspace != nullptr && (size_t)ks_req * N * M * sizeof(float) <= ws_bytes &&
+                      g.num_kb >= 2 * ks_req))
+    return set_error("gemm: K-sliced partial output needs the swap-AB single-sub-tile schedule and workspace room "
+                     "(use gemm_pick_ksplit)");
+  if (swap && MT == 1 && ks_use > 1 && workspace != nullptr && !glu && rope == nullptr && push == nullptr &&
+      (size_t)ks_use * N * M * sizeof(float) <= ws_bytes && g.num_kb >= 2 * ks_use) {
+    g.ksplit = ks_use;
+    g.streamk = 0;
+    g.part = reinterpret_cast<float*>(workspace);
+    g.part_slice = (long long)N * M;
+    const int units = g.total_tiles * g.ksplit;
+    clusters = units < slots ? units : slots;
   }
   if (clusters < 1) clusters = 1;
   g.ws = reinterpret_cast<float*>(workspace);

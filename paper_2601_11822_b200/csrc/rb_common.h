@@ -83,6 +83,9 @@ struct GemmPush {
   unsigned* done_local;  // this GEMM's CTA completion counter (self-resetting)
 };
 
+int gemm_pick_ksplit(int O, int T, int K, int num_sms, size_t ws_bytes);
+int add_partials_rmsnorm_launch(const float* part, int ks, long long slice, void* x, const void* w, void* y, int T,
+                                int H, float eps, cudaStream_t st);
 int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, const void* residual, int T,
                      int O, int K, long long ldx, long long ldw, long long ldy, int mode, int num_sms,
                      void* workspace, size_t ws_bytes, int* counters, int counters_len, cudaStream_t stream,

@@ -37,10 +37,12 @@ _SIGS = {
     "rb_debug_pattn_tiles": ([_c_int], _c_int),
     "rb_debug_decode_kv_one_op": ([_c_int], _c_int),
     "rb_debug_decode_attn_shape": ([_c_int], _c_int),
+    "rb_debug_gemm_ksplit": ([_c_int], _c_int),
     "rb_debug_stream_read": ([_vp, ctypes.c_longlong, _c_int, _c_int, _c_int, _vp, _vp], _c_int),
     "rb_debug_stream_read_tma": ([_vp, ctypes.c_longlong, _c_int, _c_int, _c_int, _c_int, _vp, _vp], _c_int),
     "rb_set_pdl": ([_c_int], _c_int),
     "rb_set_decode_glu": ([_c_int], _c_int),
+    "rb_set_decode_ksplit": ([_c_int], _c_int),
     "rb_gemm_bf16": (
         [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _c_int, _c_ll, _c_ll, _c_ll, _c_int, _c_int, _vp, _c_size, _vp,
          _c_int, _vp],

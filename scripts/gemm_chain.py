@@ -51,6 +51,7 @@ def main():
     ap.add_argument("--shapes", default="qkv,o,gate_up,down")
     ap.add_argument("--variant", type=int, default=-1)
     ap.add_argument("--pair", type=int, default=-1, help="-1 auto, 0 single CTA, 1 CTA pair")
+    ap.add_argument("--ksplit", default="0", help="K-slice unit counts to sweep (0 = the default schedule)")
     args = ap.parse_args()
     lib = ops.load()
     lib.rb_debug_gemm_variant(args.variant)
@@ -60,7 +61,7 @@ def main():
     else:
         gs = ops.GreenSplit(args.sms)
         st, sms = gs.streams[0], gs.sms[0]
-    sc = ops.GemmScratch("cuda")
+    sc = ops.GemmScratch("cuda", ws_bytes=128 << 20)
     for name in args.shapes.split(","):
         O, K = SHAPES[name]
         ws = [(torch.randn(O, K, device="cuda") * 0.02).bfloat16() for _ in range(args.n)]
@@ -69,12 +70,15 @@ def main():
             y = torch.empty(B, O, device="cuda", dtype=torch.bfloat16)
             ours = [lambda w=w: ops.linear(x, w, out=y, mode=2, num_sms=sms, scratch=sc, stream=st) for w in ws]
             cub = [lambda w=w: torch.matmul(x, w.t(), out=y) for w in ws]
-            t_ours = chain_time(ours, st) / args.n
             t_cub = chain_time(cub, st) / args.n
             wb = O * K * 2
-            print(json.dumps({"shape": name, "B": B, "sms": sms, "us": round(t_ours, 2),
-                              "tbs": round(wb / t_ours / 1e6, 2), "cublas_us": round(t_cub, 2),
-                              "cublas_tbs": round(wb / t_cub / 1e6, 2)}), flush=True)
+            for ks in (int(k) for k in args.ksplit.split(",")):
+                lib.rb_debug_gemm_ksplit(ks)
+                t_ours = chain_time(ours, st) / args.n
+                lib.rb_debug_gemm_ksplit(0)
+                print(json.dumps({"shape": name, "B": B, "sms": sms, "ksplit": ks, "us": round(t_ours, 2),
+                                  "tbs": round(wb / t_ours / 1e6, 2), "cublas_us": round(t_cub, 2),
+                                  "cublas_tbs": round(wb / t_cub / 1e6, 2)}), flush=True)
         del ws
 
 

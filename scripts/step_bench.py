@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--pdl", default="1,0")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--model", default="llama3.1-8b")
+    ap.add_argument("--ksplit", default="1", help="decode O/down K-slice partials: 1 on (default), 0 stream-K")
     args = ap.parse_args()
     lib = ops.load()
     arch = ARCHS[args.model]
@@ -61,8 +62,9 @@ def main():
             r.prefill(Bmax, ids, 0, num_sms=gs.sms[1], stream=ps.cuda_stream)
 
     out = []
-    for pdl in [int(x) for x in args.pdl.split(",")]:
+    for pdl, ks in [(int(x), int(k)) for x in args.pdl.split(",") for k in args.ksplit.split(",")]:
         lib.rb_set_pdl(pdl)
+        lib.rb_set_decode_ksplit(ks)
         lib.rb_set_decode_glu(int(os.environ.get("RB_DECODE_GLU", "0")))
         for B in Bs:
             with torch.cuda.stream(ds):
@@ -72,7 +74,7 @@ def main():
             with torch.cuda.graph(g, stream=ds):
                 r.decode_body(B, num_sms=gs.sms[0], max_pages=mp, stream=ds.cuda_stream)
             ds.synchronize()
-            res = {"pdl": pdl, "B": B, "ctx": args.ctx, "T": args.T, "decode_sms": gs.sms[0], "prefill_sms": gs.sms[1]}
+            res = {"pdl": pdl, "ksplit": ks, "B": B, "ctx": args.ctx, "T": args.T, "decode_sms": gs.sms[0], "prefill_sms": gs.sms[1]}
             for mode in ("alone", "concurrent"):
                 dts, pts = [], []
                 for _ in range(args.reps):

@@ -252,3 +252,53 @@ def test_two_layer_model_forward(name):
             # the id is the argmax of the GPU's own logits row (sampling kernel)
             assert tok == int(row.argmax()), (name, s, k)
     print(name, errs)
+
+
+@pytest.mark.parametrize("name", ["llama3.1-8b", "qwen2.5-14b"])
+@pytest.mark.parametrize("sms", [48, 72, 148])
+def test_decode_ksplit_partials_match_streamk(name, sms):
+    """Decode O / down projections as K-slice units summed in the following RMSNorm
+    (rb_set_decode_ksplit(1), the default) against the stream-K + residual-epilogue path, at the
+    real layer shapes and a bucket of 192 rows (2 real sequences + padding), on 48 / 72 / 148
+    SMs; both against the fp32 oracle."""
+    from oracle.llama_fp32 import Oracle, init_state
+    from paper_2601_11822_b200 import ops
+    from paper_2601_11822_b200.model import DecoderWeights, Runner
+
+    lib = ops.load()
+    arch = _two_layer(name)
+    st = init_state(arch, seed=2, style="random")
+    orc = Oracle(arch, st)
+    r = Runner(DecoderWeights.from_state(arch, st), num_blocks=512, num_slots=4, max_blocks_per_seq=64,
+               max_prefill_tokens=512, max_decode_batch=256)
+    g = torch.Generator().manual_seed(5)
+    lens = [300, 201]
+    prompts = []
+    for s, P in enumerate(lens):
+        prompt = torch.randint(0, arch.vocab, (P,), generator=g, dtype=torch.int32)
+        prompts.append(prompt)
+        r.block_table[s, :64] = torch.arange(64 * s, 64 * (s + 1), dtype=torch.int32).cuda()
+        r.prefill(s, prompt[: P - 1].cuda(), 0, num_sms=148)
+    bucket = 192
+    d = r.dec
+    out = {}
+    for mode in (0, 1):
+        assert lib.rb_set_decode_ksplit(mode) == 0
+        for s, P in enumerate(lens):
+            r.last_tok[s] = int(prompts[s][P - 1])
+        d.slot[:bucket] = torch.tensor([0, 1] + [r.dummy_slot] * (bucket - 2), dtype=torch.int32).cuda()
+        d.pos[:bucket] = torch.tensor([lens[0] - 1, lens[1] - 1] + [-1] * (bucket - 2), dtype=torch.int32).cuda()
+        d.seq[:bucket] = torch.tensor([lens[0], lens[1]] + [0] * (bucket - 2), dtype=torch.int32).cuda()
+        r.decode_body(bucket, num_sms=sms)
+        torch.cuda.synchronize()
+        out[mode] = (d.logits[:2].float().cpu(), [int(x) for x in d.out_ids[:2].cpu()])
+    lib.rb_set_decode_ksplit(1)
+    # the two paths round differently (stream-K adds the residual to the bf16-rounded projection,
+    # the K-slice consumer in fp32): bf16-level agreement, and each against the oracle below
+    assert rel_l2(out[1][0], out[0][0]) < 3e-2, (name, sms)
+    for s, P in enumerate(lens):
+        ref, _ = orc.forward(prompts[s].long(), 0, None)
+        e0, e1 = rel_l2(out[0][0][s], ref[P - 1]), rel_l2(out[1][0][s], ref[P - 1])
+        assert e1 <= max(TOL, 1.1 * e0 + 1e-3), (name, sms, s, e0, e1)  # no worse than the stream-K path
+        for mode in (0, 1):
+            assert out[mode][1][s] == int(out[mode][0][s].argmax())
