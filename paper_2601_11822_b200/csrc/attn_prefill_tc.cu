@@ -35,7 +35,7 @@ constexpr int kD = 128;
 constexpr int kBMq = 128;                  // query rows per CTA
 constexpr int kBN = 64;                    // keys per tile
 constexpr int kPage = 16;
-constexpr int kStages = 3;
+constexpr int kStages = 4;
 constexpr int kQBytes = 2 * kBMq * 128;    // two 64-dim halves, 16 KB each
 constexpr int kKVHalf = kBN * 128;         // 8 KB: 64 keys x 64 dims
 constexpr int kKVStage = 4 * kKVHalf;      // K lo, K hi, V lo, V hi = 32 KB
@@ -108,8 +108,7 @@ __global__ void __launch_bounds__(pattn_threads(kTiles), 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sQ = smem;                                   // [kTiles][32 KB]
   uint8_t* sKV = sQ + kTiles * kQBytes;
-  uint8_t* sP = sKV + kStages * kKVStage;               // [kTiles][2][16 KB]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + kTiles * 2 * kPBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + kStages * kKVStage);
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;
   uint64_t* kv_empty = kv_full + kStages;
@@ -158,7 +157,7 @@ __global__ void __launch_bounds__(pattn_threads(kTiles), 1)
     }
     for (int i = 0; i < 2 * kTiles; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 4);
+      mbar_init(&s_free[i], 1);  // PV of the P aliased onto this S buffer has completed
       mbar_init(&p_full[i], 4);
       mbar_init(&p_free[i], 1);
       mbar_init(&o_full[i], 1);
@@ -247,15 +246,16 @@ __global__ void __launch_bounds__(pattn_threads(kTiles), 1)
         const uint32_t vb = smem_u32(sKV + (size_t)st * kKVStage + 2 * kKVHalf);
         mbar_wait(&p_full[2 * w + b], (uint32_t)((j >> 1) & 1));  // also orders any O rescale
         tc_fence_after();
-        const uint32_t pa = smem_u32(sP + (size_t)(2 * w + b) * kPBytes);
+        // P_j (bf16, K-major) sits in the first 32 columns of S buffer b: A operand from TMEM,
+        // 16 keys = 8 columns per MMA
 #pragma unroll
         for (int kk = 0; kk < kBN / 16; ++kk) {
-          const uint64_t ad = sdesc_kmajor(pa + kk * 32);
           const uint64_t bd = sdesc_mnmajor(vb + kk * 2048, kKVHalf);
-          umma_bf16(tmem + o_col(w), ad, bd, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          umma_bf16_ts(tmem + o_col(w), tmem + s_col(w, b) + (uint32_t)(kk * 8), bd, idesc_o,
+                       (j > 0 || kk > 0) ? 1u : 0u);
         }
         umma_commit(&o_full[2 * w + b]);
-        umma_commit(&p_free[2 * w + b]);
+        umma_commit(&s_free[2 * w + b]);  // S buffer b (and the P in it) free for S_{j+2}
         umma_commit(&kv_empty[st]);
       }
       // key tiles past this query tile's diagonal (the short tile of a mirrored pair): release
@@ -295,9 +295,6 @@ __global__ void __launch_bounds__(pattn_threads(kTiles), 1)
           s[32 + i] = __uint_as_float(t1[i]);
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[2 * w + b]);
       const int kbase = j * kBN;
       // masked scores are -inf (exp2 -> 0 with no select); tile 0 always holds key 0 <= qpos,
       // so the max is finite from the first tile on. Only tiles crossing this row's diagonal
@@ -357,14 +354,12 @@ __global__ void __launch_bounds__(pattn_threads(kTiles), 1)
         pq[i & 3] += p;
       }
       l += (pq[0] + pq[1]) + (pq[2] + pq[3]);
-      // P row -> smem (K-major SW128: row r at (r/8)*1024 + (r%8)*128, 16-B chunk c at c ^ (r%8))
-      mbar_wait(&p_free[2 * w + b], ph2 ^ 1);
-      uint8_t* prow = sP + (size_t)(2 * w + b) * kPBytes + (row >> 3) * 1024 + (row & 7) * 128;
+      // P row -> TMEM over this row's S (already in registers): bf16 pairs, K-major
+      {
+        uint32_t pk[32];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const uint4 v = make_uint4(pack_bf16x2(s[8 * c + 0], s[8 * c + 1]), pack_bf16x2(s[8 * c + 2], s[8 * c + 3]),
-                                   pack_bf16x2(s[8 * c + 4], s[8 * c + 5]), pack_bf16x2(s[8 * c + 6], s[8 * c + 7]));
-        *reinterpret_cast<uint4*>(prow + ((c ^ (row & 7)) << 4)) = v;
+        for (int c = 0; c < 32; ++c) pk[c] = pack_bf16x2(s[2 * c], s[2 * c + 1]);
+        tmem_st_32x32b_x32(tmem + lane_off + s_col(w, b), pk);
       }
       if (kbase + kBN > chunk_end) {
         // keys past the chunk in its last page may never have been written (non-finite bit
@@ -381,7 +376,9 @@ __global__ void __launch_bounds__(pattn_threads(kTiles), 1)
           *reinterpret_cast<uint4*>(p) = make_uint4(0u, 0u, 0u, 0u);
         }
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the zeroed V rows (generic -> async)
+      tmem_st_wait();
+      tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[2 * w + b]);
     }
@@ -462,7 +459,7 @@ int prefill_attention_tc_launch(const void* q, long long q_tok_stride, const voi
   const int nqb = (T + kBMq - 1) / kBMq;
   int tiles = (nqb >= 2 && ((nqb + 1) / 2) * Hq >= 96) ? 2 : 1;
   if (g_pattn_tiles == 1 || (g_pattn_tiles == 2 && nqb >= 2)) tiles = g_pattn_tiles;
-  const int smem = tiles * (kQBytes + 2 * kPBytes) + kStages * kKVStage + (2 * kStages + 1 + 10 * tiles) * 8 + 16 +
+  const int smem = tiles * kQBytes + kStages * kKVStage + (2 * kStages + 1 + 10 * tiles) * 8 + 16 +
                    1024;
   using Fn = void (*)(const CUtensorMap, const CUtensorMap, const int*, int, int, int, int, __nv_bfloat16*, long long,
                       float);
