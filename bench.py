@@ -13,7 +13,7 @@ duration_s=S, seed=42, mean_prompt_tokens=1024, mean_output_tokens=256, sigma=0)
 request i served by replica i mod N (replicas.shard_items), each replica the real-time RAPID
 engine (prefill and decode of different requests concurrently on disjoint SM partitions over
 one shared paged KV cache) with the measured ARM (profiles/arm/; default policy
-"balanced", tables re-measured in round 2 with both phases strictly under load)
+"feedback", tables re-measured in round 2 with both phases strictly under load)
 choosing the green-context split at every launch. `--decode-sms 72` runs cfg 2 (static
 green-context 50/50 split), `--arm` the reference cost-model allocate(), `--engine
 hybrid-2048` the same engine's chunked-prefill comparator as the primary arm.
@@ -459,7 +459,7 @@ def main():
     ap.add_argument("--arm-profile", default="auto",
                     help="measured B200 ARM tables (profiler.py JSON; 'auto' = the committed profile of --model "
                          "under profiles/arm/)")
-    ap.add_argument("--arm-policy", default="balanced", choices=["balanced", "slo-min", "adaptive", "feedback"])
+    ap.add_argument("--arm-policy", default="feedback", choices=["balanced", "slo-min", "adaptive", "feedback"])
     ap.add_argument("--arm", action="store_true",
                     help="the reference allocate() on the cost model instead of the measured ARM")
     ap.add_argument("--arm-calibrated", default=None,

@@ -39,7 +39,6 @@ constexpr int kStages = 4;
 constexpr int kQBytes = 2 * kBMq * 128;    // two 64-dim halves, 16 KB each
 constexpr int kKVHalf = kBN * 128;         // 8 KB: 64 keys x 64 dims
 constexpr int kKVStage = 4 * kKVHalf;      // K lo, K hi, V lo, V hi = 32 KB
-constexpr int kPBytes = kBMq * kBN * 2;    // 16 KB
 constexpr int kThreads = 192;
 constexpr int kTmemCols = 256;             // S[2] x 64 + O x 128
 constexpr uint32_t kSCol = 0, kOCol = 128;
@@ -355,11 +354,14 @@ __global__ void __launch_bounds__(pattn_threads(kTiles), 1)
       }
       l += (pq[0] + pq[1]) + (pq[2] + pq[3]);
       // P row -> TMEM over this row's S (already in registers): bf16 pairs, K-major
-      {
-        uint32_t pk[32];
+      // (four 8-column stores: the packed row is never live at once next to s[], which keeps
+      // the 11-warp kernel within its 168 registers)
 #pragma unroll
-        for (int c = 0; c < 32; ++c) pk[c] = pack_bf16x2(s[2 * c], s[2 * c + 1]);
-        tmem_st_32x32b_x32(tmem + lane_off + s_col(w, b), pk);
+      for (int q4 = 0; q4 < 4; ++q4) {
+        uint32_t pk[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) pk[c] = pack_bf16x2(s[16 * q4 + 2 * c], s[16 * q4 + 2 * c + 1]);
+        tmem_st_32x32b_x8(tmem + lane_off + s_col(w, b) + (uint32_t)(8 * q4), pk);
       }
       if (kbase + kBN > chunk_end) {
         // keys past the chunk in its last page may never have been written (non-finite bit
