@@ -81,7 +81,7 @@ class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw,power.limit")
 
     def __init__(self, index: int):
         self.index = index
@@ -100,7 +100,7 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
         out, _ = self.proc.communicate(timeout=10)
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, pw, plim = [], None, set(), [], None
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
             f = [x.strip() for x in line.split(",")]
@@ -111,11 +111,16 @@ class ClockSampler:
                 mx = float(f[1])
             except ValueError:
                 continue
-            for n, v in zip(names, f[2:]):
+            for n, v in zip(names, f[2:6]):
                 if v.lower() == "active":
                     reasons.add(n)
+            try:
+                pw.append(float(f[6]))
+                plim = float(f[7])
+            except (IndexError, ValueError):
+                pass
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "power_w": statistics.median(pw) if pw else None, "power_limit_w": plim}
 
 
 def dist_setup(backend: str = "nccl"):
@@ -395,6 +400,14 @@ def serve(args, arch, items, horizon, engine_kind, rank, world, local, *, primar
     return res
 
 
+def _tpj(m):
+    """Output tokens per joule over the timed window: window tokens/s / median board power."""
+    c = m.get("clocks") or {}
+    if not m.get("complete") or not c.get("power_w") or not m.get("ms"):
+        return None
+    return round(m["tokens"] / (m["ms"] / 1e3) / c["power_w"], 3)
+
+
 def _gap_stats(log):
     """Host time per decode step: from a step's completion handling to the next launch."""
     if not log:
@@ -664,6 +677,7 @@ def main():
                      "peak_src": peaks["_src"]},
         "gpu_launches": m["launches"],
         "clocks": m["clocks"] or {"sm_mhz": None, "sm_max_mhz": None, "reasons": []},
+        "tokens_per_joule": _tpj(m),
         "cpu_baseline": cpu,
         "run_wall_s": m["run_wall_s"],
         "arm_decisions": m["arm_decisions"],
@@ -683,6 +697,7 @@ def main():
             "mean_decode_batch": comp["mean_batch"], "run_wall_s": comp["run_wall_s"],
             "max_batch": args.compare_max_batch,
             "clocks": comp["clocks"],
+            "tokens_per_joule": _tpj(comp),
             "note": "same trace, same engine code, same run; chunked-prefill hybrid batching on the whole device"}
         cv = constrained(cp)
         line["vs_comparator"] = value / cv if cv else None
