@@ -133,6 +133,8 @@ def dist_setup(backend: str = "nccl"):
         import torch
         import torch.distributed as dist
 
+        if backend == "nccl" and torch.cuda.device_count() < int(os.environ.get("LOCAL_WORLD_SIZE", world)):
+            backend = "gloo"  # more ranks than GPUs (path validation on a one-GPU box): share the devices
         if backend == "nccl":
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -350,9 +352,10 @@ def serve(args, arch, items, horizon, engine_kind, rank, world, local, *, primar
         by_part[s][1] += m
         by_part[s][2] += 1
     if world > 1:
-        t = torch.tensor([ms, host_s, pb, pm], dtype=torch.float64, device="cuda")
+        cdev = "cuda" if torch.distributed.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([ms, host_s, pb, pm], dtype=torch.float64, device=cdev)
         torch.distributed.all_reduce(t[:2], op=torch.distributed.ReduceOp.MAX)
-        tk = torch.tensor([tokens, pb, pm], dtype=torch.float64, device="cuda")
+        tk = torch.tensor([tokens, pb, pm], dtype=torch.float64, device=cdev)
         torch.distributed.all_reduce(tk, op=torch.distributed.ReduceOp.SUM)
         ms, host_s, tokens, pb, pm = float(t[0]), float(t[1]), float(tk[0]), float(tk[1]), float(tk[2])
     pooled = pool_window_stats(local_window_stats(engine.requests, slo, loop.horizon_us), pool=world > 1)
