@@ -21,6 +21,8 @@ ap.add_argument("--T", type=int, default=1023)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--decode-sms", type=int, default=72)
 ap.add_argument("--what", default="both")
+ap.add_argument("--no-green", action="store_true", help="full-device streams, grids sized for the partition "
+                "(Nsight Compute cannot profile green-context launches)")
 args = ap.parse_args()
 arch = ARCHS["llama3.1-8b"]
 w = DecoderWeights.random(arch, device="cuda")
@@ -31,8 +33,14 @@ r.kv.normal_()
 bt = torch.arange(args.B * nbps, dtype=torch.int32, device="cuda").view(args.B, nbps)
 r.block_table[: args.B] = bt
 r.block_table[args.B] = torch.arange(args.B * nbps, args.B * nbps + nbps, dtype=torch.int32, device="cuda")
-gs = ops.GreenSplit(args.decode_sms)
-ds, ps = gs.streams
+if args.no_green:
+    class _Split:  # grid sizes of the split, ordinary streams
+        sms = (args.decode_sms, 148 - args.decode_sms)
+    gs = _Split()
+    ds, ps = torch.cuda.Stream(), torch.cuda.Stream()
+else:
+    gs = ops.GreenSplit(args.decode_sms)
+    ds, ps = gs.streams
 d = r.dec
 d.slot[: args.B] = torch.arange(args.B, dtype=torch.int32, device="cuda")
 d.pos[: args.B] = args.ctx - 1
