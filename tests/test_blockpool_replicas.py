@@ -157,7 +157,11 @@ def _replica_worker(rank, world, port, q):
     toks = sum(len(r.token_times_us) for r in res.engine.requests)
     fin = sum(1 for r in res.engine.requests if r.state.value == "finished")
     agg = reduce_stats(ReplicaStats(toks, 6.0, fin, res.summary.itl_p99_us, res.summary.ttft_p50_us))
-    q.put((rank, toks, fin, agg))
+    from paper_2601_11822_b200.replicas import local_window_stats, pool_window_stats
+
+    local = local_window_stats(res.engine.requests, SloSpec(itl_slo_us=50_000), 6_000_000)
+    pooled = pool_window_stats(local)  # what bench.py reports at N > 1
+    q.put((rank, toks, fin, agg, local, pooled))
     dist.destroy_process_group()
 
 
@@ -183,6 +187,19 @@ def test_replicas_gloo_world2():
     out.sort()
     tot = sum(o[1] for o in out)
     fin = sum(o[2] for o in out)
-    for _, _, _, agg in out:
+    for _, _, _, agg, _, _ in out:
         assert agg["tokens"] == tot and agg["finished"] == fin
         assert agg["window_s"] == 6.0
+    # bench's pooled run-level stats: whole-job tokens / the common window, and the p99 ITL /
+    # p50 TTFT over the UNION of both replicas' samples (not a max of per-rank percentiles)
+    from paper_2601_11822_b200.slo import percentile_nearest_rank
+
+    locs = [o[4] for o in out]
+    gaps = [g for l in locs for g in l["gaps"]]
+    ttfts = [t for l in locs for t in l["ttfts"]]
+    for o in out:
+        pooled = o[5]
+        assert pooled["replicas"] == 2
+        assert pooled["tokens_per_s"] == sum(l["stamps"] for l in locs) / locs[0]["window_s"]
+        assert pooled["itl_p99_us"] == percentile_nearest_rank(gaps, 99.0)
+        assert pooled["ttft_p50_us"] == percentile_nearest_rank(ttfts, 50.0)
