@@ -12,8 +12,9 @@ offline), one B200 per replica, synthetic trace `synthesize(WorkloadSpec(qps=Q*N
 duration_s=S, seed=42, mean_prompt_tokens=1024, mean_output_tokens=256, sigma=0))` with
 request i served by replica i mod N (replicas.shard_items), each replica the real-time RAPID
 engine (prefill and decode of different requests concurrently on disjoint SM partitions over
-one shared paged KV cache) with the measured ARM (profiles/arm/; default policy
-"feedback", tables re-measured in round 2 with both phases strictly under load)
+one shared paged KV cache) with the measured ARM (profiles/arm/; default policy per
+model: "feedback" for 8B, "balanced" for Qwen-14B; tables re-measured in round 2 with both phases
+strictly under load)
 choosing the green-context split at every launch. `--decode-sms 72` runs cfg 2 (static
 green-context 50/50 split), `--arm` the reference cost-model allocate(), `--engine
 hybrid-2048` the same engine's chunked-prefill comparator as the primary arm.
@@ -64,6 +65,10 @@ SLO_ITL_US = 50_000
 PROMPT, OUTPUT = 1024, 256
 # measured ARM tables (python -m paper_2601_11822_b200.profiler), per model, at its benchmark mix
 DEFAULT_PROFILES = {"llama3.1-8b": "llama3.1-8b_ctx1152_chunk1023_r02.json", "qwen2.5-14b": "qwen2.5-14b_ctx8256.json"}
+# measured-ARM policy per model (same-box runs, profiles/r02/): 8B 1024/256 — feedback beats balanced by
+# 3-5% (time-shares the 32/64-SM hull pair); Qwen-14B 8192/128 — balanced (32 decode SMs) 438 tok/s,
+# feedback settles on 56 and starves prefill (355)
+DEFAULT_POLICY = {"llama3.1-8b": "feedback", "qwen2.5-14b": "balanced"}
 
 
 def _peaks() -> dict:
@@ -475,7 +480,8 @@ def main():
     ap.add_argument("--arm-profile", default="auto",
                     help="measured B200 ARM tables (profiler.py JSON; 'auto' = the committed profile of --model "
                          "under profiles/arm/)")
-    ap.add_argument("--arm-policy", default="feedback", choices=["balanced", "slo-min", "adaptive", "feedback"])
+    ap.add_argument("--arm-policy", default=None, choices=["balanced", "slo-min", "adaptive", "feedback"],
+                    help="measured-ARM policy (default: per model, DEFAULT_POLICY)")
     ap.add_argument("--arm", action="store_true",
                     help="the reference allocate() on the cost model instead of the measured ARM")
     ap.add_argument("--arm-calibrated", default=None,
@@ -498,6 +504,8 @@ def main():
             args.arm = True
     if args.arm_profile:
         args.arm = True
+    if args.arm_policy is None:
+        args.arm_policy = DEFAULT_POLICY.get(args.model, "balanced")
     if args.decode_sms is None:
         args.decode_sms = 72
 
