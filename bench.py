@@ -64,7 +64,7 @@ sys.path.insert(0, ROOT)
 SLO_ITL_US = 50_000
 PROMPT, OUTPUT = 1024, 256
 # measured ARM tables (python -m paper_2601_11822_b200.profiler), per model, at its benchmark mix
-DEFAULT_PROFILES = {"llama3.1-8b": "llama3.1-8b_ctx1152_chunk1023_r02.json", "qwen2.5-14b": "qwen2.5-14b_ctx8256.json"}
+DEFAULT_PROFILES = {"llama3.1-8b": "llama3.1-8b_ctx1152_chunk1023_r02.json", "qwen2.5-14b": "qwen2.5-14b_ctx8256_r02.json"}
 # measured-ARM policy per model (same-box runs, profiles/r02/): 8B 1024/256 — feedback beats balanced by
 # 3-5% (time-shares the 32/64-SM hull pair); Qwen-14B 8192/128 — balanced (32 decode SMs) 438 tok/s,
 # feedback settles on 56 and starves prefill (355)
@@ -386,6 +386,8 @@ def serve(args, arch, items, horizon, engine_kind, rank, world, local, *, primar
                   "by_sms": {str(k): {"gbs": v[0] / v[1] / 1e6 if v[1] else None, "launches": v[2]}
                              for k, v in sorted(by_part.items())}},
         "host_gap": _gap_stats(getattr(ex, "host_gap_log", [])),
+        "host_prof": ({k: round(v / max(1, ex.host_prof["steps"]) / 1e3, 1) for k, v in ex.host_prof.items()
+                       if k != "steps"} if getattr(ex, "host_prof", None) else None),
         "duty": {"decode": duty([(g, ns) for _, g, ns in ex.step_log], w0, w1),
                  "prefill": duty(getattr(ex, "prefill_log", []), w0, w1)},
         "run_wall_s": t_run, "requests": len(engine.requests),
@@ -693,7 +695,8 @@ def main():
         "run_wall_s": m["run_wall_s"],
         "arm_decisions": m["arm_decisions"],
         "stream_duty": m["duty"],
-        "host_loop": {"decode_completion_to_next_launch": m["host_gap"], "poll_sleep_us": args.poll_sleep_us},
+        "host_loop": {"decode_completion_to_next_launch": m["host_gap"], "poll_sleep_us": args.poll_sleep_us,
+                      "us_per_step_by_stage": m["host_prof"]},
         "requests": m["requests"],
         "finished": m["finished_all"],
         "profiles": os.path.join(ROOT, "profiles"),

@@ -155,6 +155,9 @@ class B200Executor:
         self.step_log: list[tuple[int, int, int]] = []  # (B, gpu_us, host launch ns)
         self.host_gap_log: list[int] = []  # us from a decode completion's handling to the next launch
         self._t_fin_ns = None
+        # RB_HOST_PROFILE=1: ns spent per decode step in finish_decode / launch composition / command issue
+        self.host_prof = {"finish": 0, "compose": 0, "issue": 0, "steps": 0} if os.environ.get("RB_HOST_PROFILE") \
+            else None
         self.prefill_log: list[tuple[int, int]] = []  # (gpu_us, host launch ns)
         # in-situ decode-attention roofline: (algorithmic K+V bytes, kernel ms, decode SMs, host
         # launch ns) of the probed layer in every decode step (CUDA events inside the graphs)
@@ -399,6 +402,7 @@ class B200Executor:
         self.lazy_captures = 0  # captures counted from here on happened while serving
 
     def launch_decode(self, members, decision, co_prefill_chunk) -> GpuHandle:
+        t_prof = time.perf_counter_ns() if self.host_prof is not None else 0
         part = self._pick(decision)
         B = len(members)
         bucket = self._bucket(B)
@@ -413,8 +417,15 @@ class B200Executor:
             slots += [self.runner.dummy_slot] * pad
             pos += [-1] * pad
             seq += [0] * pad
+        if t_prof:
+            t_mid = time.perf_counter_ns()
         self._issue(("decode", self._partition_key(part), self._take_updates("decode"), B, bucket, slots, pos, seq))
         h.finish_record(part.ds)
+        if t_prof:
+            t_end = time.perf_counter_ns()
+            self.host_prof["compose"] += t_mid - t_prof
+            self.host_prof["issue"] += t_end - t_mid
+            self.host_prof["steps"] += 1
         if self._t_fin_ns is not None:  # host time from the previous step's completion to this launch
             self.host_gap_log.append((time.perf_counter_ns() - self._t_fin_ns) // 1000)
             self._t_fin_ns = None
@@ -442,6 +453,8 @@ class B200Executor:
             # the step's end event has completed, so this step's probe records are final
             self.attn_probe_log.append((handle.attn_bytes, self._probe_events[0].elapsed_time(self._probe_events[1]),
                                         handle.d_sms, handle.launch_ns))
+        if self.host_prof is not None:
+            self.host_prof["finish"] += time.perf_counter_ns() - self._t_fin_ns
 
     # ------------------------------------------------------------------ hybrid (K9 fused iteration)
     def launch_hybrid(self, members, head, written, chunk, target):
