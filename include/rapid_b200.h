@@ -27,6 +27,12 @@
 extern "C" {
 #endif
 
+/* Host path: stream-ordered copy (pinned host <-> device, cudaMemcpyDefault) and the launch of an
+ * instantiated CUDA graph (the decode step's captured forward) on a stream — one C call each on the
+ * per-step issue path instead of the framework's tensor copy / graph-replay dispatch. */
+int rb_memcpy_async(void* dst, const void* src, size_t bytes, void* stream);
+int rb_graph_launch(void* graph_exec, void* stream);
+
 /* Library identity / diagnostics. */
 const char* rb_version(void);
 const char* rb_last_error(void);

@@ -133,6 +133,17 @@ int rb_argmax(const void* logits, long long ld, int T, int V, int* out, const in
   return rb::argmax_launch(logits, ld, T, V, out, slot_of_row, last_tok, row_valid, ST(stream));
 }
 
+int rb_memcpy_async(void* dst, const void* src, size_t bytes, void* stream) {
+  if (bytes == 0) return 0;
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? 0 : rb::set_cuda_error("rb_memcpy_async", e);
+}
+
+int rb_graph_launch(void* graph_exec, void* stream) {
+  cudaError_t e = cudaGraphLaunch(static_cast<cudaGraphExec_t>(graph_exec), static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? 0 : rb::set_cuda_error("rb_graph_launch", e);
+}
+
 int rb_block_table_update(const int* upd, int* block_table, int bt_stride, int max_updates, void* stream) {
   return rb::bt_update_launch(upd, block_table, bt_stride, max_updates, ST(stream));
 }

@@ -27,6 +27,7 @@ import os
 import sys
 import time
 
+import numpy as np
 import torch
 
 from paper_2601_11822_b200 import ops
@@ -40,10 +41,11 @@ MAX_UPDATES = 1 << 16
 
 
 class GpuHandle:
-    def __init__(self, kind, stream, cu_fraction):
+    def __init__(self, kind, stream, cu_fraction, events=None):
         self.kind = kind
-        self.ev0 = torch.cuda.Event(enable_timing=True)
-        self.ev1 = torch.cuda.Event(enable_timing=True)
+        # (executor-pooled) start / end events: creating two CUDA events per launch cost ~10-20 us of host time
+        self.ev0, self.ev1 = events if events is not None else (torch.cuda.Event(enable_timing=True),
+                                                                torch.cuda.Event(enable_timing=True))
         self.ev0.record(stream)
         self.gpu_us = 0
         self.cu_fraction = cu_fraction
@@ -71,6 +73,8 @@ class _Partition:
         self.p_sms = prefill_sms
         self.green = green
         self.graphs: dict[int, torch.cuda.CUDAGraph] = {}
+        self.graph_exec: dict[int, int] = {}  # bucket -> cudaGraphExec_t of graphs[bucket]
+        self.key = None  # decode SM count this partition is registered under (None = full device)
 
 
 class B200Executor:
@@ -124,6 +128,12 @@ class B200Executor:
                          for k in self._upd}
         self._dec_in_host = torch.zeros(3, max_batch, dtype=torch.int32, pin_memory=True)
         self._dec_in_host_np = self._dec_in_host.numpy()
+        self._dec_in_bytes = self._dec_in_host.numel() * 4
+        self._lib = ops.load()
+        self._ev_pool: list = []
+        self._upd_host_np = {k: v.numpy() for k, v in self._upd_host.items()}
+        self._bt_ptr = self.runner.block_table.data_ptr()
+        self._bt_stride = self.runner.block_table.stride(0)
         self._dec_in_dev = torch.zeros(3, max_batch, dtype=torch.int32, device=self.device)
         d = self.runner.dec
         d.slot = self._dec_in_dev[0]
@@ -188,7 +198,9 @@ class B200Executor:
     def _partition(self, decode_sms: int | None) -> _Partition:
         if decode_sms not in self._partitions:
             gs = ops.GreenSplit(decode_sms, device=self.device.index or 0)
-            self._partitions[decode_sms] = _Partition(gs.streams[0], gs.streams[1], gs.sms[0], gs.sms[1], gs)
+            p = _Partition(gs.streams[0], gs.streams[1], gs.sms[0], gs.sms[1], gs)
+            p.key = decode_sms
+            self._partitions[decode_sms] = p
         return self._partitions[decode_sms]
 
     def _pick(self, decision: AllocationDecision) -> _Partition:
@@ -234,14 +246,15 @@ class B200Executor:
         n = len(q)
         if n > MAX_UPDATES:
             raise RuntimeError("too many pending block-table updates")
-        h = self._upd_host[phase]
+        h = self._upd_host_np[phase]
         h[0] = n
-        flat = torch.tensor(q, dtype=torch.int32).view(-1)
-        h[1 : 1 + 3 * n].copy_(flat)
+        h[1 : 1 + 3 * n] = np.asarray(q, dtype=np.int32).reshape(-1)
         d = self._upd_dev[phase]
-        with torch.cuda.stream(stream):
-            d[: 1 + 3 * n].copy_(h[: 1 + 3 * n], non_blocking=True)
-        ops.block_table_update(d, self.runner.block_table, n, stream=stream)
+        lib = self._lib
+        ops._check(lib.rb_memcpy_async(d.data_ptr(), self._upd_host[phase].data_ptr(), 4 * (1 + 3 * n),
+                                       stream.cuda_stream), "rb_memcpy_async")
+        ops._check(lib.rb_block_table_update(d.data_ptr(), self._bt_ptr, self._bt_stride, n, stream.cuda_stream),
+                   "rb_block_table_update")
         self.h2d_bytes += 4 * (1 + 3 * n)
         self.gpu_launches += 1
         q.clear()  # one launch per phase is in flight, so the pinned buffer is free again at the next flush
@@ -273,7 +286,15 @@ class B200Executor:
     command_sink = None  # callable(cmd) or None
 
     def _partition_key(self, part: _Partition) -> int | None:
-        return next(k for k, v in self._partitions.items() if v is part)
+        return part.key
+
+    def _events(self):
+        return self._ev_pool.pop() if self._ev_pool else None
+
+    def _recycle(self, handle) -> None:
+        # a handle someone still holds for timing (bench's window marks, h._win) keeps its events
+        if handle is not None and not getattr(handle, "_win", False) and len(self._ev_pool) < 64:
+            self._ev_pool.append((handle.ev0, handle.ev1))
 
     def run_command(self, cmd) -> _Partition:
         """Execute one device command (the same on every TP rank); returns its partition."""
@@ -304,14 +325,28 @@ class B200Executor:
             h[0, :bucket] = slots
             h[1, :bucket] = pos
             h[2, :bucket] = seq
-            with torch.cuda.stream(st):
-                self._dec_in_dev[:, :bucket].copy_(self._dec_in_host[:, :bucket], non_blocking=True)
-                if self.use_graphs:
-                    self._capture(part, bucket).replay()
-                else:
+            lib, sh = self._lib, st.cuda_stream
+            # the whole [3, max_batch] staging block (3 KB at 256 rows): one contiguous copy; rows past
+            # the bucket are never read by the bucket's graph
+            ops._check(lib.rb_memcpy_async(self._dec_in_dev.data_ptr(), self._dec_in_host.data_ptr(),
+                                           self._dec_in_bytes, sh), "rb_memcpy_async")
+            if self.use_graphs:
+                g = self._capture(part, bucket)
+                ex_h = part.graph_exec.get(bucket)
+                if ex_h is None:
+                    raw = g.raw_cuda_graph_exec()
+                    ex_h = part.graph_exec[bucket] = raw if isinstance(raw, int) else 0
+                if ex_h:
+                    ops._check(lib.rb_graph_launch(ex_h, sh), "rb_graph_launch")
+                else:  # no raw handle from this torch build: the framework's replay
+                    with torch.cuda.stream(st):
+                        g.replay()
+            else:
+                with torch.cuda.stream(st):
                     self.runner.decode_body(bucket, num_sms=part.d_sms, max_pages=(max(seq) + PAGE - 1) // PAGE,
-                                            stream=st.cuda_stream)
-                self._dec_out_host[:B].copy_(self.runner.dec.out_ids[:B], non_blocking=True)
+                                            stream=sh)
+            ops._check(lib.rb_memcpy_async(self._dec_out_host.data_ptr(), self.runner.dec.out_ids.data_ptr(), 4 * B,
+                                           sh), "rb_memcpy_async")
             self.h2d_bytes += 12 * bucket
             self.d2h_bytes += 4 * B
             self.gpu_launches += self.runner.kernels_per_forward(bucket, 0, True, False, True)
@@ -331,7 +366,7 @@ class B200Executor:
 
     def launch_prefill(self, req, written: int, chunk: int, target: int, decision, co_decode) -> GpuHandle:
         part = self._pick(decision)
-        h = GpuHandle("prefill", part.ps, part.p_sms / self.total_sms)
+        h = GpuHandle("prefill", part.ps, part.p_sms / self.total_sms, self._events())
         slot = self._slot_of[req.id]
         lo, hi = written, min(written + chunk, target - 1)
         ids = self._context_ids(req, lo, hi).tolist() if hi > lo else []
@@ -345,6 +380,7 @@ class B200Executor:
     def finish_prefill(self, handle) -> None:
         if handle is not None:
             self.prefill_log.append((handle.gpu_us, handle.launch_ns))
+            self._recycle(handle)
 
     # ------------------------------------------------------------------ decode
     def _bucket(self, B: int) -> int:
@@ -406,7 +442,7 @@ class B200Executor:
         part = self._pick(decision)
         B = len(members)
         bucket = self._bucket(B)
-        h = GpuHandle("decode", part.ds, part.d_sms / self.total_sms)
+        h = GpuHandle("decode", part.ds, part.d_sms / self.total_sms, self._events())
         slot_of = self._slot_of
         seq = [r.prompt_tokens + len(r.token_times_us) for r in members]  # context_tokens (core.py:98-101)
         slots = [slot_of[r.id] for r in members]
@@ -453,6 +489,7 @@ class B200Executor:
             # the step's end event has completed, so this step's probe records are final
             self.attn_probe_log.append((handle.attn_bytes, self._probe_events[0].elapsed_time(self._probe_events[1]),
                                         handle.d_sms, handle.launch_ns))
+        self._recycle(handle)
         if self.host_prof is not None:
             self.host_prof["finish"] += time.perf_counter_ns() - self._t_fin_ns
 

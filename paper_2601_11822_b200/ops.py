@@ -38,6 +38,8 @@ _SIGS = {
     "rb_debug_decode_kv_one_op": ([_c_int], _c_int),
     "rb_debug_decode_attn_shape": ([_c_int], _c_int),
     "rb_debug_gemm_ksplit": ([_c_int], _c_int),
+    "rb_memcpy_async": ([_vp, _vp, ctypes.c_size_t, _vp], _c_int),
+    "rb_graph_launch": ([_vp, _vp], _c_int),
     "rb_debug_stream_read": ([_vp, ctypes.c_longlong, _c_int, _c_int, _c_int, _vp, _vp], _c_int),
     "rb_debug_stream_read_tma": ([_vp, ctypes.c_longlong, _c_int, _c_int, _c_int, _c_int, _vp, _vp], _c_int),
     "rb_set_pdl": ([_c_int], _c_int),
