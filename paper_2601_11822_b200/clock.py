@@ -175,6 +175,9 @@ class RealTimeLoop:
         virtual-clock replay reproduces with (arrival, seq) / (completion, seq) ordering
         (tests/test_trace_replay.py)."""
         self._t0 = time.perf_counter_ns()
+        # idle hook of the engine's executor (off-critical-path bookkeeping while GPU work runs)
+        owner = getattr(handler, "__self__", None)
+        on_idle = getattr(getattr(owner, "executor", None), "on_idle", None)
         while self._timed or self._pending:
             now = self.clock_us()
             done = []
@@ -199,6 +202,8 @@ class RealTimeLoop:
                     self.now_us = now
                     self._dispatch(ev, handler)
             if not progressed:
+                if on_idle is not None:
+                    on_idle()
                 if not self._pending and self._timed:
                     wait = self._timed[0][0] - self.clock_us()
                     if wait > 200:

@@ -140,9 +140,11 @@ class B200Executor:
         d.pos = self._dec_in_dev[1]
         d.seq = self._dec_in_dev[2]
         self._dec_out_host = torch.zeros(max_batch, dtype=torch.int32, pin_memory=True)
+        self._dec_out_host_np = self._dec_out_host.numpy()
         self._pre_ids_host = torch.zeros(max(chunk_tokens, 16), dtype=torch.int32, pin_memory=True)
         self._pre_ids_dev = torch.zeros(max(chunk_tokens, 16), dtype=torch.int32, device=self.device)
-        self.generated: dict[int, list[int]] = {}
+        self._generated: dict[int, list[int]] = {}
+        self._pending_gen: list = []  # (members, lame, ids) of finished steps not yet in _generated
         # parity tests: fp32 host copy of the logits row behind every generated token
         self.record_logits = record_logits
         self.logits: dict[int, list[torch.Tensor]] = {}
@@ -473,17 +475,41 @@ class B200Executor:
         self.decode_steps += 1
         return h
 
+    @property
+    def generated(self) -> dict[int, list[int]]:
+        """Sampled ids per request (prompt excluded), in order."""
+        self._drain_generated()
+        return self._generated
+
+    def _drain_generated(self) -> None:
+        pend, self._pending_gen = self._pending_gen, []
+        gen = self._generated
+        for members, lame, ids in pend:
+            for r, is_lame, tok in zip(members, lame, ids.tolist()):
+                if not is_lame:
+                    gen.setdefault(r.id, []).append(tok)
+
+    def on_idle(self) -> None:
+        """The real-time loop's idle hook (no event ready): bookkeeping that is off the critical path."""
+        if self._pending_gen:
+            self._drain_generated()
+
     def finish_decode(self, handle) -> None:
         if handle is None:
             return
         self._t_fin_ns = time.perf_counter_ns()
-        out = self._dec_out_host[: len(handle.members)].tolist()
-        rows = self.runner.dec.logits[: len(handle.members)].float().cpu() if self.record_logits else None
-        for i, (r, is_lame, tok) in enumerate(zip(handle.members, handle.lame, out)):
-            if not is_lame:
-                self.generated.setdefault(r.id, []).append(tok)
-                if rows is not None:
+        B = len(handle.members)
+        if self.record_logits:
+            out = self._dec_out_host[:B].tolist()
+            rows = self.runner.dec.logits[:B].float().cpu()
+            for i, (r, is_lame, tok) in enumerate(zip(handle.members, handle.lame, out)):
+                if not is_lame:
+                    self.generated.setdefault(r.id, []).append(tok)
                     self.logits.setdefault(r.id, []).append(rows[i])
+        else:
+            # the ids are snapshotted (the next step's D2H reuses the pinned buffer) and filed into
+            # `generated` when the loop idles or someone reads them (a re-prefill after preemption)
+            self._pending_gen.append((handle.members, handle.lame, self._dec_out_host_np[:B].copy()))
         self.step_log.append((len(handle.members), handle.gpu_us, handle.launch_ns))
         if self._probe_events is not None:
             # the step's end event has completed, so this step's probe records are final
