@@ -383,7 +383,8 @@ def serve(args, arch, items, horizon, engine_kind, rank, world, local, *, primar
         "mean_batch": statistics.mean(win["Bs"]) if win["Bs"] else None,
         "mean_ctx": statistics.mean(win["ctxs"]) if win["ctxs"] else None,
         "probe": {"bytes": pb, "ms": pm, "launches": len(probe),
-                  "by_sms": {str(k): {"gbs": v[0] / v[1] / 1e6 if v[1] else None, "launches": v[2]}
+                  "by_sms": {str(k): {"gbs": v[0] / v[1] / 1e6 if v[1] else None, "launches": v[2],
+                                      "bytes": v[0], "ms": v[1]}
                              for k, v in sorted(by_part.items())}},
         "host_gap": _gap_stats(getattr(ex, "host_gap_log", [])),
         "host_prof": ({k: round(v / max(1, ex.host_prof["steps"]) / 1e3, 1) for k, v in ex.host_prof.items()
@@ -624,6 +625,23 @@ def main():
         traffic = ratio * per_launch_bytes
     steps = max(1, m["steps"])
     value = constrained(pooled)
+    # Partition bound of K3: every KV byte crosses an SM's shared memory twice (TMA write, ldmatrix
+    # read) and one SM's shared memory moves 128 B per clock, so a d-SM partition streams at most
+    # d x 64 B x f_SM (profiles/r02/dattn/smem_port/). At the in-situ clock this
+    # is below HBM for partitions under ~(hbm / 64 B / f) SMs.
+    part = None
+    sm_mhz = (m["clocks"] or {}).get("sm_mhz")
+    if sm_mhz and pr["by_sms"]:
+        t_bound = t_act = 0.0
+        per = {}
+        for k, v in pr["by_sms"].items():
+            bound = min(hbm, int(k) * 64 * sm_mhz * 1e6 / 1e9)
+            per[k] = {"bound_gbs": round(bound, 1), "frac": round(v["gbs"] / bound, 3) if v["gbs"] else None}
+            if v["ms"]:
+                t_bound += v["bytes"] / (bound * 1e6)
+                t_act += v["ms"]
+        part = {"bound": "min(hbm, decode SMs x 64 B x in-situ SM clock)", "sm_mhz": sm_mhz,
+                "by_decode_sms": per, "frac": round(t_bound / t_act, 3) if t_act else None}
     line = {
         "metric": "SLO-constrained output tokens/s per GPU (p99 ITL<=SLO); p50 TTFT; p99 ITL",
         "value": value,
@@ -681,7 +699,9 @@ def main():
                      "measured": (f"in situ: CUDA events around layer {arch.layers // 2}'s decode attention inside "
                                   f"the decode graphs, {pr['launches']} launches over the K timed steps on the ARM's "
                                   f"partitions; {per_launch_bytes:.0f} algorithmic B per launch on average"),
-                     "by_decode_sms": pr["by_sms"],
+                     "by_decode_sms": {k: {"gbs": v["gbs"], "launches": v["launches"]}
+                                       for k, v in pr["by_sms"].items()},
+                     "partition_bound": part,
                      "traffic_src": "profiles/ncu_traffic.json (dram read+write / algorithmic bytes of one "
                                     "ncu --set full launch) x the mean in-situ launch bytes",
                      "isolated_full_device": (None if iso is None else

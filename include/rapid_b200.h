@@ -48,6 +48,9 @@ int rb_debug_gemm_pair_mode(int mode);
 /* Debug: decode (swap-AB) GEMM schedule, -1 auto (default); else bit0 = two 128-row weight
  * sub-tiles per activation stage, bit1 = stream-K (else data-parallel whole tiles). */
 int rb_debug_gemm_variant(int v);
+/* Debug: decode (swap-AB) GEMMs, weight k-blocks warmed into L2 ahead of the smem ring
+ * (cp.async.bulk.prefetch.tensor); -1 = auto (default), 0 = off, 1..64 = forced. */
+int rb_debug_gemm_prefetch(int kblocks);
 /* Debug: stream-K for token-major (prefill) GEMMs whose whole-tile waves quantize badly
  * (fewer than 4 waves, last wave at most max_frac full); default off (measured slower). */
 int rb_debug_gemm_prefill_streamk(int on, double max_frac);

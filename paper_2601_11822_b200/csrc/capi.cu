@@ -27,6 +27,7 @@ int prefill_attention_tc_launch(const void* q, long long q_tok_stride, const voi
 int gemm_set_trace(unsigned long long* buf);
 int gemm_set_pair_mode(int mode);
 int gemm_set_variant(int v);
+int gemm_set_prefetch(int kblocks);
 int gemm_set_prefill_streamk(int on, double max_frac);
 int gemm_set_prefill_bn(int bn);
 int prefill_attn_set_tiles(int tiles);
@@ -49,6 +50,7 @@ const char* rb_last_error(void) { return rb::last_error(); }
 int rb_debug_gemm_trace(unsigned long long* buf) { return rb::gemm_set_trace(buf); }
 int rb_debug_gemm_pair_mode(int mode) { return rb::gemm_set_pair_mode(mode); }
 int rb_debug_gemm_variant(int v) { return rb::gemm_set_variant(v); }
+int rb_debug_gemm_prefetch(int kblocks) { return rb::gemm_set_prefetch(kblocks); }
 int rb_debug_gemm_prefill_streamk(int on, double max_frac) { return rb::gemm_set_prefill_streamk(on, max_frac); }
 int rb_debug_gemm_prefill_bn(int bn) { return rb::gemm_set_prefill_bn(bn); }
 int rb_debug_pattn_tiles(int tiles) { return rb::prefill_attn_set_tiles(tiles); }

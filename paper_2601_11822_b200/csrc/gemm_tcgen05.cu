@@ -866,6 +866,12 @@ int gemm_set_prefill_streamk(int on, double max_frac) {
   g_prefill_streamk_frac = max_frac;
   return 0;
 }
+static int g_gemm_pf = -1;  // decode (swap-AB) weight k-blocks warmed into L2 ahead of the ring: -1 auto, 0 off
+int gemm_set_prefetch(int kblocks) {
+  if (kblocks < -1 || kblocks > 64) return -1;
+  g_gemm_pf = kblocks;
+  return 0;
+}
 int gemm_set_variant(int v) {
   g_force_variant = v;
   g_mt2_sets = (v >= 0 && (v & (1 << 14))) ? 2 : 1;
@@ -964,6 +970,7 @@ int gemm_bf16_launch(const void* X, const void* W, void* Y, const void* bias, co
   g.mt = MT;
   g.a_blocked = blocked;
   g.pf_dist = (variant & 4) ? 8 : 0;
+  if (swap && g_gemm_pf >= 0) g.pf_dist = g_gemm_pf;
   g.dbg = (pair == 1 && variant > 0) ? (variant >> 3) & 3 : 0;
   if (variant > 0 && (variant & (1 << 12))) g.dbg |= 4;  // debug: epilogue skips its global stores
   int KA = 1;

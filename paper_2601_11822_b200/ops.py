@@ -32,6 +32,7 @@ _SIGS = {
     "rb_debug_gemm_trace": ([_vp], _c_int),
     "rb_debug_gemm_pair_mode": ([_c_int], _c_int),
     "rb_debug_gemm_variant": ([_c_int], _c_int),
+    "rb_debug_gemm_prefetch": ([_c_int], _c_int),
     "rb_debug_gemm_prefill_streamk": ([_c_int, ctypes.c_double], _c_int),
     "rb_debug_gemm_prefill_bn": ([_c_int], _c_int),
     "rb_debug_pattn_tiles": ([_c_int], _c_int),

@@ -26,6 +26,8 @@ ap.add_argument("--sms", default="56")
 ap.add_argument("--B", type=int, default=224)
 ap.add_argument("--ctx", type=int, default=1152)
 ap.add_argument("--reps", type=int, default=40)
+ap.add_argument("--shapes", default="0", help="decode-attention ring shapes to sweep (0 auto, 1..4 = 12x2, 8x3, 6x4, 4x6)")
+ap.add_argument("--cases", default="alone,gemm,mma_only,load_only")
 args = ap.parse_args()
 ops.load()
 lib = ops.load()
@@ -55,54 +57,57 @@ for sm in [int(s) for s in args.sms.split(",")]:
         ops.decode_attention(q, cache, bt, slots, seq, out, num_kv_heads=HKV, max_pages=nbps, workspace=ws,
                              num_sms=dn, stream=ds)
 
-    with torch.cuda.stream(ds):
-        attn()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g, stream=ds):
-        for _ in range(args.reps):
+    for shape in [int(v) for v in args.shapes.split(",")]:
+        lib.rb_debug_decode_attn_shape(shape)
+        with torch.cuda.stream(ds):
             attn()
-    for case in ("alone", "gemm", "mma_only", "load_only"):
-        lib.rb_debug_gemm_pair_mode(0 if case != "gemm" else -1)
-        lib.rb_debug_gemm_variant({"alone": -1, "gemm": -1, "mma_only": 16, "load_only": 8}[case])
-        bg = None
-        if case != "alone":
-            with torch.cuda.stream(ps):
-                ops.linear(x, w, y, num_sms=pn, stream=ps)
-            torch.cuda.synchronize()
-            bg = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(bg, stream=ps):
-                for _ in range(20):
-                    ops.linear(x, w, y, num_sms=pn, stream=ps)
-        torch.cuda.synchronize()
-        clk = ClockSampler(0)
-        clk.start()
-        ts, gts = [], []
-        for _ in range(8):
-            if bg is not None:  # graph replays launch on the CURRENT stream
-                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=ds):
+            for _ in range(args.reps):
+                attn()
+        for case in args.cases.split(","):
+            lib.rb_debug_gemm_pair_mode(0 if case != "gemm" else -1)
+            lib.rb_debug_gemm_variant({"alone": -1, "gemm": -1, "mma_only": 16, "load_only": 8}[case])
+            bg = None
+            if case != "alone":
                 with torch.cuda.stream(ps):
-                    a0.record(ps)
-                    bg.replay()
-                    bg.replay()
-                    a1.record(ps)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            with torch.cuda.stream(ds):
-                e0.record(ds)
-                g.replay()
-                e1.record(ds)
+                    ops.linear(x, w, y, num_sms=pn, stream=ps)
+                torch.cuda.synchronize()
+                bg = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(bg, stream=ps):
+                    for _ in range(20):
+                        ops.linear(x, w, y, num_sms=pn, stream=ps)
             torch.cuda.synchronize()
-            ts.append(e0.elapsed_time(e1) * 1e3 / args.reps)
-            if bg is not None:
-                gts.append(a0.elapsed_time(a1) * 1e3 / 40)
-        c = clk.stop()
-        us = statistics.median(ts)
-        r = {"decode_sms": dn, "case": case, "attn_us": round(us, 1), "attn_gbs": round(attn_bytes / us / 1e3, 1),
-             "bg_gemm_us": round(statistics.median(gts), 1) if gts else None, "sm_mhz": c.get("sm_mhz"),
-             "reasons": c.get("reasons")}
-        print(json.dumps(r), flush=True)
-        res.append(r)
-        del bg
-    lib.rb_debug_gemm_variant(-1)
-    lib.rb_debug_gemm_pair_mode(-1)
-    del g
+            clk = ClockSampler(0)
+            clk.start()
+            ts, gts = [], []
+            for _ in range(8):
+                if bg is not None:  # graph replays launch on the CURRENT stream
+                    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    with torch.cuda.stream(ps):
+                        a0.record(ps)
+                        bg.replay()
+                        bg.replay()
+                        a1.record(ps)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(ds):
+                    e0.record(ds)
+                    g.replay()
+                    e1.record(ds)
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1) * 1e3 / args.reps)
+                if bg is not None:
+                    gts.append(a0.elapsed_time(a1) * 1e3 / 40)
+            c = clk.stop()
+            us = statistics.median(ts)
+            r = {"decode_sms": dn, "shape": shape, "case": case, "attn_us": round(us, 1), "attn_gbs": round(attn_bytes / us / 1e3, 1),
+                 "bg_gemm_us": round(statistics.median(gts), 1) if gts else None, "sm_mhz": c.get("sm_mhz"),
+                 "reasons": c.get("reasons")}
+            print(json.dumps(r), flush=True)
+            res.append(r)
+            del bg
+        lib.rb_debug_gemm_variant(-1)
+        lib.rb_debug_gemm_pair_mode(-1)
+        lib.rb_debug_decode_attn_shape(0)
+        del g
     gs.close()

@@ -52,6 +52,7 @@ def main():
     ap.add_argument("--variant", type=int, default=-1)
     ap.add_argument("--pair", type=int, default=-1, help="-1 auto, 0 single CTA, 1 CTA pair")
     ap.add_argument("--ksplit", default="0", help="K-slice unit counts to sweep (0 = the default schedule)")
+    ap.add_argument("--pf", default="-1", help="weight L2 lookahead k-blocks to sweep (-1 auto, 0 off)")
     args = ap.parse_args()
     lib = ops.load()
     lib.rb_debug_gemm_variant(args.variant)
@@ -72,11 +73,13 @@ def main():
             cub = [lambda w=w: torch.matmul(x, w.t(), out=y) for w in ws]
             t_cub = chain_time(cub, st) / args.n
             wb = O * K * 2
-            for ks in (int(k) for k in args.ksplit.split(",")):
+            for ks, pf in ((int(k), int(p)) for k in args.ksplit.split(",") for p in args.pf.split(",")):
                 lib.rb_debug_gemm_ksplit(ks)
+                lib.rb_debug_gemm_prefetch(pf)
                 t_ours = chain_time(ours, st) / args.n
                 lib.rb_debug_gemm_ksplit(0)
-                print(json.dumps({"shape": name, "B": B, "sms": sms, "ksplit": ks, "us": round(t_ours, 2),
+                lib.rb_debug_gemm_prefetch(-1)
+                print(json.dumps({"shape": name, "B": B, "sms": sms, "ksplit": ks, "pf": pf, "us": round(t_ours, 2),
                                   "tbs": round(wb / t_ours / 1e6, 2), "cublas_us": round(t_cub, 2),
                                   "cublas_tbs": round(wb / t_cub / 1e6, 2)}), flush=True)
         del ws
