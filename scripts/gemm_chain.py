@@ -76,6 +76,7 @@ def main():
             ws = [w.view(O // 128, 128, K // 64, 64).permute(0, 2, 1, 3).contiguous().view(O, K) for w in plain]
             mode = 2 | 8
             xc = torch.randn(128, K, device="cuda").bfloat16()
+            torch.cuda.synchronize()  # made on the default stream; the GEMMs below run on `st`
             y0 = ops.linear(xc, plain[0], mode=2, num_sms=sms, scratch=sc, stream=st)
             y1 = ops.linear(xc, ws[0], mode=mode, num_sms=sms, scratch=sc, stream=st)
             st.synchronize()
