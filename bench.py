@@ -411,6 +411,26 @@ def serve(args, arch, items, horizon, engine_kind, rank, world, local, *, primar
     return res
 
 
+def partition_bound(by_sms: dict, sm_mhz: float | None, hbm_gbs: float) -> dict | None:
+    """K3's in-situ rate against its partition bound. Every KV byte crosses an SM's shared memory
+    twice (TMA write, ldmatrix read) and one SM's shared memory moves 128 B per clock, so a d-SM
+    partition streams at most d x 64 B x f_SM (profiles/r02/dattn/smem_port/); the
+    bound is min(HBM, that). by_sms: {decode SMs: {"gbs", "bytes", "ms"}} of the timed launches;
+    "frac" = time at the bound / measured time over all of them."""
+    if not sm_mhz or not by_sms:
+        return None
+    t_bound = t_act = 0.0
+    per = {}
+    for k, v in by_sms.items():
+        bound = min(hbm_gbs, int(k) * 64 * sm_mhz * 1e6 / 1e9)
+        per[k] = {"bound_gbs": round(bound, 1), "frac": round(v["gbs"] / bound, 3) if v["gbs"] else None}
+        if v["ms"]:
+            t_bound += v["bytes"] / (bound * 1e6)
+            t_act += v["ms"]
+    return {"bound": "min(hbm, decode SMs x 64 B x in-situ SM clock)", "sm_mhz": sm_mhz, "by_decode_sms": per,
+            "frac": round(t_bound / t_act, 3) if t_act else None}
+
+
 def _tpj(m):
     """Output tokens per joule over the timed window: window tokens/s / median board power."""
     c = m.get("clocks") or {}
@@ -625,23 +645,7 @@ def main():
         traffic = ratio * per_launch_bytes
     steps = max(1, m["steps"])
     value = constrained(pooled)
-    # Partition bound of K3: every KV byte crosses an SM's shared memory twice (TMA write, ldmatrix
-    # read) and one SM's shared memory moves 128 B per clock, so a d-SM partition streams at most
-    # d x 64 B x f_SM (profiles/r02/dattn/smem_port/). At the in-situ clock this
-    # is below HBM for partitions under ~(hbm / 64 B / f) SMs.
-    part = None
-    sm_mhz = (m["clocks"] or {}).get("sm_mhz")
-    if sm_mhz and pr["by_sms"]:
-        t_bound = t_act = 0.0
-        per = {}
-        for k, v in pr["by_sms"].items():
-            bound = min(hbm, int(k) * 64 * sm_mhz * 1e6 / 1e9)
-            per[k] = {"bound_gbs": round(bound, 1), "frac": round(v["gbs"] / bound, 3) if v["gbs"] else None}
-            if v["ms"]:
-                t_bound += v["bytes"] / (bound * 1e6)
-                t_act += v["ms"]
-        part = {"bound": "min(hbm, decode SMs x 64 B x in-situ SM clock)", "sm_mhz": sm_mhz,
-                "by_decode_sms": per, "frac": round(t_bound / t_act, 3) if t_act else None}
+    part = partition_bound(pr["by_sms"], (m["clocks"] or {}).get("sm_mhz"), hbm)
     line = {
         "metric": "SLO-constrained output tokens/s per GPU (p99 ITL<=SLO); p50 TTFT; p99 ITL",
         "value": value,
@@ -731,6 +735,8 @@ def main():
             "mean_decode_batch": comp["mean_batch"], "run_wall_s": comp["run_wall_s"],
             "max_batch": args.compare_max_batch,
             "clocks": comp["clocks"],
+            "stream_duty": comp["duty"]["decode"],
+            "host_gap": comp["host_gap"],
             "tokens_per_joule": _tpj(comp),
             "note": "same trace, same engine code, same run; chunked-prefill hybrid batching on the whole device"}
         cv = constrained(cp)
