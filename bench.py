@@ -38,7 +38,9 @@ weights, ~30 GB per step), so no extra flush is needed.
 roofline: decode attention (K3), measured IN SITU: CUDA events recorded around the middle
 layer's attention launch inside every decode graph (rb_workspace_t.probe_ev*), summed over
 the K timed steps on whatever partition the ARM chose; algorithmic bytes per launch =
-sum over rows of ctx * Hkv * 128 * 2 (K,V) * 2 B.
+sum over rows of ctx * Hkv * 128 * 2 (K,V) * 2 B. `roofline.partition_bound` puts the same
+launches against min(HBM, decode SMs x 64 B x in-situ SM clock): on the small decode partitions
+the SMs' shared-memory port, not HBM, bounds K3.
 
 N > 1 (torchrun): one independent replica per GPU ("replicas only"; the path shards by
 request, no data-path collective); barrier + max-over-ranks of the device window; tokens and
